@@ -1,0 +1,5 @@
+"""CPU oracle for the DABS hot path -- TEST INFRASTRUCTURE ONLY.
+
+Importable only from tests/, ``__graft_entry__.smoke()`` and bench.py's
+cpu_baseline / ``--impl reference`` legs.  Shares no code with the product.
+"""

@@ -1,0 +1,590 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test ties the oracle to something other than itself: values printed in
+the paper or in the SPEC's worked examples (tests/golden/, cited), closed
+forms, brute force over all 2^n vectors, library routines (numpy matmul), or
+invariants that hold for any correct implementation.  A plausible mistake
+anywhere in oracle/dabs_oracle.c (a dropped term, a sign, an index, a
+transposed operand, a wrong tie-break) fails at least one of them.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+ALG_MAXMIN, ALG_CYCLIC, ALG_RANDOM, ALG_POSMIN, ALG_TWO = range(5)
+PH_STRAIGHT, PH_GREEDY, PH_MAIN = 0, 1, 2
+
+
+def qubo(n, diag, off):
+    U = np.zeros((n, n), np.int16)
+    for k, d in enumerate(diag):
+        U[k, k] = d
+    for i, j, w in off:
+        U[min(i, j), max(i, j)] = w
+    return U
+
+
+def all_x(n):
+    return np.array(list(itertools.product([0, 1], repeat=n)), np.int64)
+
+
+def E_matmul(U, X):
+    """Eq.(2) via a library matmul: with U upper triangular, x^T U x sums each
+    i<=j term once."""
+    U = U.astype(np.int64)
+    return np.einsum("bi,ij,bj->b", X, U, X)
+
+
+def rand_upper(rng, n, lo=-50, hi=50):
+    return np.triu(rng.integers(lo, hi + 1, size=(n, n))).astype(np.int16)
+
+
+# ---------------------------------------------------------------- Philox
+def test_philox_kat(orc):
+    for v in golden("philox_kat.json")["vectors"]:
+        out = orc.philox([int(h, 16) for h in v["ctr"]], [int(h, 16) for h in v["key"]])
+        assert [f"{x:08x}" for x in out] == v["out"]
+
+
+# ---------------------------------------------------------------- Eq.(2)
+def test_energy_spec_n3(orc):
+    g = golden("spec_examples.json")["n3_model"]
+    U = qubo(3, g["diag"], g["off"])
+    assert orc.energy(U, np.array([1, 1, 0])) == g["E_of_110"]
+    X = all_x(3)
+    E = [orc.energy(U, x) for x in X]
+    assert min(E) == g["optimum_E"]
+    assert list(X[int(np.argmin(E))]) == g["optimum_x"]
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 11])
+def test_energy_equals_matmul_bruteforce(orc, n):
+    rng = np.random.default_rng(100 + n)
+    U = rand_upper(rng, n, -32767, 32767)
+    X = all_x(n)
+    ref = E_matmul(U, X)
+    got = np.array([orc.energy(U, x) for x in X])
+    assert np.array_equal(got, ref)
+
+
+def test_fig1_fixture(orc):
+    """E(X) = H(S) + 6 for every S; optimum X=[1,0,0,0,1], E=-8,
+    H=-14 at S=[+1,-1,-1,-1,+1].  H from Eq.(1) directly."""
+    g = golden("fig1_fixture.json")
+    n = g["n"]
+    U = qubo(n, g["qubo_diag"], g["qubo_off"])
+    h = np.array(g["h"])
+    # Ising -> QUBO conversion written constructively, checked
+    # against the fixture's QUBO weights
+    diag = 2 * h.copy()
+    for i, j, J in g["J"]:
+        diag[i] -= 2 * J
+        diag[j] -= 2 * J
+    assert list(diag) == g["qubo_diag"]
+    for (i, j, J), (a, b, w) in zip(sorted(g["J"]), sorted(g["qubo_off"])):
+        assert (i, j, 4 * J) == (a, b, w)
+    best = None
+    for x in all_x(n):
+        s = 2 * x - 1
+        H = sum(J * s[i] * s[j] for i, j, J in g["J"]) + int((h * s).sum())
+        E = orc.energy(U, x)
+        assert E == H + g["offset_E_minus_H"]
+        if best is None or E < best[0]:
+            best = (E, H, list(x), list(s))
+    assert best[0] == g["E_opt"] and best[1] == g["H_opt"]
+    assert best[2] == g["X_opt"] and best[3] == g["S_opt"]
+
+
+# ---------------------------------------------------------------- Eq.(3)-(5)
+def test_delta_closed_form_vs_definition(orc):
+    """Eq.(3) against the definition Delta_k = E(f_k X) - E(X)."""
+    rng = np.random.default_rng(7)
+    for _ in range(100):
+        n = int(rng.integers(1, 10))
+        U = rand_upper(rng, n)
+        x = rng.integers(0, 2, n)
+        e0 = E_matmul(U, x[None])[0]
+        ref = []
+        for k in range(n):
+            y = x.copy()
+            y[k] ^= 1
+            ref.append(E_matmul(U, y[None])[0] - e0)
+        assert list(orc.delta_closed(U, x)) == ref
+
+
+def test_spec_init_and_flip(orc):
+    g = golden("spec_examples.json")["n3_model"]
+    U = qubo(3, g["diag"], g["off"])
+    st = orc.SlotState.initial(U)
+    assert list(st.delta) == g["init_delta"]          # Delta_k = W_kk at X=0
+    orc.step_flip(U, st, 0)
+    assert st.E == g["after_flip0_E"]
+    assert list(st.delta) == g["after_flip0_delta"]
+    assert list(st.x) == [1, 0, 0]
+
+
+def test_incremental_update_random_walk(orc):
+    """Eqs.(4)-(5) over 3000 random flips match the definition at every step."""
+    rng = np.random.default_rng(11)
+    n = 13
+    U = rand_upper(rng, n, -32767, 32767)
+    st = orc.SlotState.initial(U)
+    for _ in range(3000):
+        i = int(rng.integers(0, n))
+        before = st.copy()
+        orc.step_flip(U, st, i)
+        x = st.x.astype(np.int64)
+        assert st.E == E_matmul(U, x[None])[0]
+        assert st.E == before.E + before.delta[i]                  # Step 3
+        for k in range(n):
+            y = x.copy()
+            y[k] ^= 1
+            assert st.delta[k] == E_matmul(U, y[None])[0] - st.E
+    # double flip restores the state exactly (Eq.(5) twice)
+    s0 = st.copy()
+    orc.step_flip(U, st, 3)
+    orc.step_flip(U, st, 3)
+    assert np.array_equal(st.x, s0.x) and np.array_equal(st.delta, s0.delta) and st.E == s0.E
+
+
+# ---------------------------------------------------------------- rules
+def phases(res):
+    return list(zip(res.trace_phase.tolist(), res.trace_bit.tolist()))
+
+
+def test_straight_spec_trace(orc):
+    """from 000 to 110 Straight flips bit 0 (Delta=-3) then bit 1."""
+    g = golden("spec_examples.json")["n3_model"]
+    U = qubo(3, g["diag"], g["off"])
+    st = orc.SlotState.initial(U)
+    r = orc.batch(U, st, np.array([1, 1, 0]), ALG_CYCLIC, T=1, B=1, trace_cap=100)
+    straight = [b for p, b in phases(r) if p == PH_STRAIGHT]
+    assert straight == g["straight_000_to_110_bits"]
+
+
+def test_greedy_spec_n2(orc):
+    g = golden("spec_examples.json")["n2_greedy"]
+    U = qubo(2, g["diag"], g["off"])
+    st = orc.SlotState.initial(U)
+    r = orc.batch(U, st, np.array([0, 0]), ALG_CYCLIC, T=1, B=1, trace_cap=100, tabu=0)
+    ph = phases(r)
+    first_greedy = []
+    for p, b in ph:
+        if p >= PH_MAIN:
+            break
+        first_greedy.append(b)
+    assert first_greedy == g["greedy_bits"]
+    assert r.trace_E[0] == g["final_E"]
+    st2 = orc.SlotState.initial(U)
+    orc.step_flip(U, st2, 0)
+    assert list(st2.x) == g["final_x"] and list(st2.delta) == g["final_delta"]
+
+
+def test_twoneighbor_paper_trace(orc):
+    """from X=000000 TwoNeighbor flips 0,1,0,2,1,3,2,4,3,5,4 and
+    passes through the listed states."""
+    g = golden("twoneighbor_n6.json")
+    n = g["n"]
+    rng = np.random.default_rng(3)
+    U = rand_upper(rng, n, -5, 5)
+    for k in range(n):
+        U[k, k] = 100          # X = 0 is a strict local minimum: no Greedy flips
+    st = orc.SlotState.initial(U)
+    r = orc.batch(U, st, np.zeros(n, np.uint8), ALG_TWO, T=1, B=1, trace_cap=1000)
+    ph = phases(r)
+    main = [b for p, b in ph if p >= PH_MAIN]
+    assert main == g["bits"]
+    assert all(p == PH_MAIN for p, _ in ph[: len(g["bits"])])
+    x = np.zeros(n, np.int64)
+    for b, s in zip(g["bits"], g["states"]):
+        x[b] ^= 1
+        assert "".join(map(str, x)) == s
+
+
+def ball2_min(U, x):
+    n = len(x)
+    best = E_matmul(U, x[None])[0]
+    for i in range(n):
+        for j in range(i, n):
+            y = x.copy()
+            y[i] ^= 1
+            if j != i:
+                y[j] ^= 1
+            best = min(best, E_matmul(U, y[None])[0])
+    return best
+
+
+def test_twoneighbor_covers_2ball(orc):
+    """TwoNeighbor scans every 2-bit neighbour of its start X, so
+    E(BEST) <= min E over the Hamming ball of radius 2 around that X."""
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        n = int(rng.integers(2, 12))
+        U = rand_upper(rng, n)
+        st = orc.SlotState.initial(U)
+        st.x[:] = rng.integers(0, 2, n)
+        st.delta[:] = orc.delta_closed(U, st.x)
+        st.E = int(E_matmul(U, st.x[None].astype(np.int64))[0])
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        x0 = st.x.copy().astype(np.int64)
+        r = orc.batch(U, st, D, ALG_TWO, T=1, B=1, trace_cap=10000)
+        # replay to the TwoNeighbor start
+        x = x0.copy()
+        for p, b in phases(r):
+            if p >= PH_MAIN:
+                break
+            x[b] ^= 1
+        assert r.ebest <= ball2_min(U, x)
+        assert r.ebest == E_matmul(U, r.best[None].astype(np.int64))[0]
+
+
+def test_positivemin_spec_candidates(orc):
+    """with Delta=[-2,3,5] only bits 0 and 1 are candidates.
+    Build a diagonal model whose current Delta is exactly that."""
+    g = golden("spec_examples.json")["positivemin_candidates"]
+    U = qubo(3, g["delta"], [])
+    chosen = set()
+    for seed in range(200):
+        st = orc.SlotState.initial(U)
+        # X=0: Delta = diag = [-2,3,5].  Tabu 0; one PositiveMin flip is the
+        # first MAIN flip only if Straight/Greedy do nothing, so start at the
+        # local minimum instead: x=[1,0,0] -> Delta=[2,3,5]; use D = x.
+        st.x[:] = [1, 0, 0]
+        st.delta[:] = orc.delta_closed(U, st.x)
+        st.E = -2
+        r = orc.batch(U, st, np.array([1, 0, 0]), ALG_POSMIN, T=1, B=1, tabu=0, seed=seed, trace_cap=50)
+        first_main = next(b for p, b in phases(r) if p >= PH_MAIN)
+        chosen.add(first_main)
+    # at x=[1,0,0] Delta=[2,3,5]: posmin = 2 -> candidates {0}; check rule form:
+    assert chosen == {0}
+    # and the SPEC's own vector through the same rule at X=0 with D=0 is not
+    # reachable (Greedy would move first); the candidate-set arithmetic is
+    # pinned by the frequency test below.
+
+
+def test_positivemin_frequencies(orc):
+    """Uniform pick among {k : Delta_k <= posmin}."""
+    # diagonal model at its local minimum with Delta = [4, 4, 9, 4]
+    U = qubo(4, [-4, -4, -9, -4], [])
+    counts = np.zeros(4, int)
+    for seed in range(4000):
+        st = orc.SlotState.initial(U)
+        st.x[:] = 1
+        st.delta[:] = orc.delta_closed(U, st.x)
+        st.E = -21
+        r = orc.batch(U, st, np.ones(4, np.uint8), ALG_POSMIN, T=1, B=1, tabu=0, seed=seed, trace_cap=50)
+        counts[next(b for p, b in phases(r) if p >= PH_MAIN)] += 1
+    assert counts[2] == 0
+    for k in (0, 1, 3):
+        assert abs(counts[k] - 4000 / 3) < 5 * np.sqrt(4000 * (1 / 3) * (2 / 3))
+
+
+def test_maxmin_at_t_equals_T_is_argmin_uniform(orc):
+    """at t=T, D(T)=minDelta, so the flip is uniform over the minima."""
+    U = qubo(3, [0, 0, -10], [])
+    counts = np.zeros(3, int)
+    for seed in range(3000):
+        st = orc.SlotState.initial(U)
+        st.x[:] = [0, 0, 1]
+        st.delta[:] = orc.delta_closed(U, st.x)   # [0, 0, 10]
+        st.E = -10
+        r = orc.batch(U, st, np.array([0, 0, 1]), ALG_MAXMIN, T=1, B=1, tabu=0, seed=seed, trace_cap=20)
+        counts[next(b for p, b in phases(r) if p >= PH_MAIN)] += 1
+    assert counts[2] == 0
+    assert abs(counts[0] - 1500) < 5 * np.sqrt(3000 * 0.25)
+
+
+def test_checked_mode_all_algorithms(orc):
+    """Delta recomputed from scratch (direct energy differences for n<=64,
+    Eq.(3) above) equals the incremental Delta after every flip, for every
+    rule, over consecutive batches on a persistent slot."""
+    rng = np.random.default_rng(21)
+    for n in (1, 2, 7, 24, 90):
+        U = rand_upper(rng, n, -300, 300)
+        for algo in range(5):
+            st = orc.SlotState.initial(U)
+            for gen in range(3):
+                D = rng.integers(0, 2, n).astype(np.uint8)
+                T = orc.flip_factor(100, n)
+                B = orc.flip_factor(1000, n)
+                r = orc.batch(U, st, D, algo, T=T, B=B, seed=5, slot=3, gen=gen, checked=True)
+                assert r.ebest == E_matmul(U, r.best[None].astype(np.int64))[0]
+                assert st.delta.min() >= 0          # batches end in Greedy
+
+
+def test_batch_structure_and_budget(orc):
+    """Straight, Greedy, then (main, Greedy) rounds;
+    each non-TwoNeighbor main run is exactly T flips; the budget is tested at
+    round boundaries: every round but the last starts below B, the total
+    reaches B.  TwoNeighbor runs once (2n-1 flips)."""
+    rng = np.random.default_rng(8)
+    n = 150
+    U = rand_upper(rng, n, -1000, 1000)
+    T, B = orc.flip_factor(600, n), orc.flip_factor(2000, n)
+    assert (T, B) == (90, 300)
+    for algo in range(5):
+        st = orc.SlotState.initial(U)
+        for gen in range(2):
+            D = rng.integers(0, 2, n).astype(np.uint8)
+            ham = int((st.x != D).sum())
+            r = orc.batch(U, st, D, algo, T=T, B=B, seed=9, gen=gen, trace_cap=100000)
+            ph = r.trace_phase.tolist()
+            assert len(ph) == r.flips
+            # run-length encode phases
+            runs = []
+            for p in ph:
+                if runs and runs[-1][0] == p:
+                    runs[-1][1] += 1
+                else:
+                    runs.append([p, 1])
+            i = 0
+            if runs and runs[0][0] == PH_STRAIGHT:
+                assert runs[0][1] == ham
+                i = 1
+            else:
+                assert ham == 0
+            if i < len(runs) and runs[i][0] == PH_GREEDY:
+                i += 1
+            mains = []
+            cum = sum(r[1] for r in runs[:i])
+            while i < len(runs):
+                assert runs[i][0] == PH_MAIN + len(mains)
+                mains.append((cum, runs[i][1]))
+                cum += runs[i][1]
+                i += 1
+                if i < len(runs) and runs[i][0] == PH_GREEDY:
+                    cum += runs[i][1]
+                    i += 1
+            assert len(mains) >= 1
+            if algo == ALG_TWO:
+                assert len(mains) == 1 and mains[0][1] == 2 * n - 1
+            else:
+                assert all(m[1] == T for m in mains)
+                # every round starts below the budget; the whole batch reaches it
+                assert all(start < B for start, _ in mains)
+                assert r.flips >= B
+
+
+def test_paper_budget_example_arithmetic(orc):
+    """The worked example P:529-531: n=1000, s=0.6, b=2.0 -> T=600, B=2000
+    (integer flip factors, R-13)."""
+    assert orc.flip_factor(600, 1000) == 600
+    assert orc.flip_factor(2000, 1000) == 2000
+    assert orc.flip_factor(1100, 100) == 110      # where double ceil(1.1*100) gives 111
+    assert orc.flip_factor(100, 16) == 2 and orc.flip_factor(10000, 16) == 160
+
+
+# ---------------------------------------------------------------- GA
+def test_rank_bias(orc):
+    """the first row is chosen with probability m^(-1/3);
+    SPEC S:439: r=0.5, m=100 -> the 13th row (0-based 12)."""
+    m = 100
+    assert orc.rank_pick(1 << 31, m) == 12
+    assert orc.rank_pick(0, m) == 0 and orc.rank_pick(0xFFFFFFFF, m) == m - 1
+    lo, hi = 0, 0xFFFFFFFF          # largest u with rank 0
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        if orc.rank_pick(mid, m) == 0:
+            lo = mid
+        else:
+            hi = mid - 1
+    assert abs((lo + 1) / 2**32 - m ** (-1 / 3)) < 1e-9
+
+
+def test_genops(orc):
+    g = golden("spec_examples.json")["interval_zero_wrap"]
+    n = g["n"]
+    ones = np.ones(n, np.uint8)
+    D = orc.build_target(5, ones, ones, ones, seed=1, gslot=0, gen=0, L=g["L"], start=g["start"])
+    cleared = set(np.flatnonzero(D == 0).tolist())
+    want = set()
+    for a, b in g["cleared"]:
+        want |= set(range(a, b + 1))
+    assert cleared == want
+    rng = np.random.default_rng(2)
+    n = 20000
+    A = rng.integers(0, 2, n).astype(np.uint8)
+    Bv = rng.integers(0, 2, n).astype(np.uint8)
+    best0 = rng.integers(0, 2, n).astype(np.uint8)
+    kw = dict(seed=3, gslot=7, gen=2)
+    assert np.array_equal(orc.build_target(6, A, Bv, best0, **kw), best0)          # Best
+    mut = orc.build_target(0, A, Bv, best0, **kw)                                    # Mutation
+    assert abs((mut != A).mean() - 1 / 8) < 0.01
+    cx = orc.build_target(1, A, Bv, best0, **kw)                                     # Crossover
+    assert np.all((cx == A) | (cx == Bv))
+    assert abs((cx[A != Bv] == A[A != Bv]).mean() - 0.5) < 0.02
+    assert np.array_equal(orc.build_target(1, A, A, best0, **kw), A)
+    z = orc.build_target(3, np.ones(n, np.uint8), Bv, best0, **kw)                  # Zero
+    assert abs((z == 0).mean() - 1 / 8) < 0.01
+    o = orc.build_target(4, np.zeros(n, np.uint8), Bv, best0, **kw)                 # One
+    assert abs((o == 1).mean() - 1 / 8) < 0.01
+    rnd = orc.build_target(7, A, Bv, best0, **kw)                                    # Random
+    assert abs(rnd.mean() - 0.5) < 0.02
+
+
+def test_adaptive_choice_mixture(orc):
+    """with probability eps a uniform genop / algorithm, else the tag
+    of a uniform pool row.  Expected P(g) = (1-eps) frac_g + eps/8."""
+    rng = np.random.default_rng(4)
+    n = 12
+    U = rand_upper(rng, n)
+    cfg = orc.Config(s_milli=100, b_milli=100, pools=1, slots=6000, cap=100)
+    w = orc.World(U, cfg)
+    w.reset(77)
+    pool0 = w.pool(0)
+    fg = np.bincount(pool0["genop"], minlength=8) / 100
+    fa = np.bincount(pool0["algo"], minlength=5) / 100
+    w.generation_local()
+    d, _ = w.stats()
+    d = d[0].astype(float)
+    N = 6000
+    pg = 0.95 * fg + 0.05 / 8
+    pa = 0.95 * fa + 0.05 / 5
+    got_g = d.sum(0) / N
+    got_a = d.sum(1) / N
+    for p, q in zip(pg, got_g):
+        assert abs(p - q) < 5 * np.sqrt(p * (1 - p) / N) + 1e-9
+    for p, q in zip(pa, got_a):
+        assert abs(p - q) < 5 * np.sqrt(p * (1 - p) / N) + 1e-9
+
+
+# ---------------------------------------------------------------- reductions
+def test_maxcut_reduction_exhaustive(orc):
+    from paper_2207_03069_b200 import workloads as wl
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        n = int(rng.integers(2, 10))
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        m = int(rng.integers(1, len(pairs) + 1))
+        idx = rng.choice(len(pairs), m, replace=False)
+        edges = np.array([pairs[k] for k in idx], np.int64)
+        w = rng.choice([-1, 1, 3], m)
+        U = wl.maxcut_qubo(n, edges, w)
+        for x in all_x(n):
+            cut = sum(int(ww) for (a, b), ww in zip(edges, w) if x[a] != x[b])
+            assert orc.energy(U, x) == -cut
+
+
+def test_qap_reduction(orc):
+    from paper_2207_03069_b200 import workloads as wl
+    g = golden("spec_examples.json")["qap_n2"]
+    U = wl.qap_qubo(np.array(g["flow"]), np.array(g["dist"]), g["p"])
+    E = [orc.energy(U, x) for x in all_x(4)]
+    assert min(E) == g["feasible_E"]
+    assert orc.energy(U, np.array([1, 0, 0, 1])) == g["feasible_E"]
+    assert orc.energy(U, np.array([0, 1, 1, 0])) == g["feasible_E"]
+    rng = np.random.default_rng(13)
+    m = 3
+    for _ in range(5):
+        flow = rng.integers(0, 6, (m, m))
+        dist = rng.integers(0, 6, (m, m))
+        np.fill_diagonal(flow, 0)
+        np.fill_diagonal(dist, 0)
+        p = 60
+        U = wl.qap_qubo(flow, dist, p)
+        for x in all_x(m * m):
+            M = x.reshape(m, m)
+            E = orc.energy(U, x)
+            if (M.sum(0) == 1).all() and (M.sum(1) == 1).all():
+                gmap = M.argmax(1)
+                C = sum(flow[i, j] * dist[gmap[i], gmap[j]] for i in range(m) for j in range(m))
+                assert E == C - m * p
+            else:
+                assert E >= -(m - 1) * p
+
+
+def test_tsp_penalty_and_cycle_optimum(orc):
+    """R-22: p = 4 max d + 1 makes the QUBO optimum a tour (brute force m=4);
+    cycle-metric optimum C* = 2 m scale (permutation enumeration m<=7)."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, d, p, E_star = wl.tsp_onehot(4, 10, seed=3)
+    E = E_matmul(U, all_x(16))
+    assert E.min() == E_star
+    flow = wl.circular_flow(4)
+    for m in range(4, 8):
+        d = wl.cycle_metric(m, 10, seed=m)
+        flow = wl.circular_flow(m)
+        best = min(sum(flow[i, j] * d[g[i], g[j]] for i in range(m) for j in range(m))
+                   for g in itertools.permutations(range(m)))
+        assert best == 2 * m * 10
+
+
+# ---------------------------------------------------------------- world
+def test_world_invariants(orc):
+    rng = np.random.default_rng(31)
+    n = 40
+    U = rand_upper(rng, n, -100, 100)
+    cfg = orc.Config(s_milli=200, b_milli=1000, pools=2, slots=5, cap=16)
+    sysm = orc.System(U, cfg, world=1, checked=True)
+    sysm.reset(5)
+    w = sysm.ranks[0]
+    prev_best = orc.E_INF
+    for g in range(6):
+        sysm.generation()
+        for p in range(cfg.pools):
+            pool = w.pool(p)
+            keys = list(zip(pool["E"].tolist(), pool["seq"].tolist()))
+            assert keys == sorted(keys)
+            fin = pool["E"] != orc.E_INF
+            seen = set()
+            for X, E in zip(pool["X"][fin], pool["E"][fin]):
+                assert E == E_matmul(U, X[None].astype(np.int64))[0]
+                key = (int(E), X.tobytes())
+                assert key not in seen
+                seen.add(key)
+        E, X, rec = w.best()
+        assert E <= prev_best
+        prev_best = E
+        assert E == E_matmul(U, X[None].astype(np.int64))[0]
+        for s in range(cfg.pools * cfg.slots):
+            st = w.slot(s)
+            assert st.E == E_matmul(U, st.x[None].astype(np.int64))[0]
+            assert np.array_equal(st.delta, orc.delta_closed(U, st.x))
+    d, ins = w.stats()
+    assert d.sum() == 6 * cfg.pools * cfg.slots
+    assert (ins <= d).all()
+
+
+def bruteforce_min(U):
+    n = U.shape[0]
+    X = all_x(n)
+    return int(E_matmul(U, X).min())
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_k16_single_search_finds_optimum(orc, seed):
+    """Config K16: one search, one pool, s=0.1, b=10; the run reaches the
+    brute-force optimum over all 65536 vectors."""
+    from paper_2207_03069_b200 import workloads as wl
+    U = wl.random_dense(16, seed)
+    opt = bruteforce_min(U)
+    cfg = orc.Config(s_milli=100, b_milli=10000, pools=1, slots=1)
+    sysm = orc.System(U, cfg)
+    E, X, rec = sysm.run(seed=seed, flip_budget=10**7, target=opt)
+    assert E == opt
+    assert E == E_matmul(U, X[None].astype(np.int64))[0]
+
+
+def test_small_random_instances_reach_optimum(orc):
+    """SPEC acceptance 1 style: random n in [4,16], weights in [-8,8]."""
+    rng = np.random.default_rng(41)
+    hits = 0
+    for trial in range(30):
+        n = int(rng.integers(4, 17))
+        U = rand_upper(rng, n, -8, 8)
+        opt = bruteforce_min(U)
+        cfg = orc.Config(s_milli=100, b_milli=1000, pools=1, slots=4)
+        E, X, _ = orc.System(U, cfg).run(seed=trial, flip_budget=200000, target=opt)
+        hits += int(E == opt)
+    assert hits >= 29
+
+
+def test_tsp_small_reaches_pinned_optimum(orc):
+    from paper_2207_03069_b200 import workloads as wl
+    U, d, p, E_star = wl.tsp_onehot(5, 10, seed=2)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=2, slots=8)
+    E, X, _ = orc.System(U, cfg).run(seed=1, flip_budget=5 * 10**6, target=E_star)
+    assert E == E_star
