@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py -- bit-flips/s of the B200 DABS hot path (arXiv 2207.03069).
+
+One step = one generation of the whole hot path: GA seeding
+of every slot, one batch search per slot (Straight, Greedy, main rounds), pool
+merge, exchange.  `value` = box-wide flips in the K timed steps / device time
+(CUDA events on the library's stream, max over ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload R32K|K2000s|TSP32|GS800|K16]
+    python bench.py --impl reference ...   # the CPU oracle on the host cores
+
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; one rank per GPU,
+NCCL all-gather of the pool snapshot per generation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "bit-flips/sec per GPU and box at 1/2/4/8 B200; time-to-target QUBO energy"
+UNIT = "flips/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dabs", choices=["dabs", "reference"])
+    ap.add_argument("--workload", default="R32K", choices=["K16", "GS800", "TSP32", "K2000s", "R32K"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample size (cpu_baseline)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_sample(U, meta, seconds: float, seed: int):
+    """Time the CPU oracle (as it stands) on host cores: one thread per core,
+    each a persistent slot from X=0 running batches (random target, algorithm
+    = thread mod 5, like generation 0 of the GPU run, where every pool row is a
+    random sentinel) until its share of flips is done.  Returns (flips, s, cores)."""
+    from oracle import oracle as orc
+    orc.lib()
+    n = U.shape[0]
+    cores = os.cpu_count() or 1
+    T, B = orc.flip_factor(meta["s_milli"], n), orc.flip_factor(meta["b_milli"], n)
+    # calibrate the per-flip cost on one thread
+    st = orc.SlotState.initial(U)
+    D = orc.build_target(7, np.zeros(n, np.uint8), np.zeros(n, np.uint8), np.zeros(n, np.uint8),
+                         seed=seed, gslot=10**6, gen=0)
+    t0 = time.perf_counter()
+    f = orc.batch_sample(U, st, D, 1, T=T, B=B, tabu=8, seed=seed, slot=10**6, gen=0,
+                         flip_limit=max(20, 2_000_000 // max(n, 1)))
+    per_flip = (time.perf_counter() - t0) / max(f, 1)
+    quota = max(50, int(seconds / per_flip))
+    results = [0] * cores
+
+    def worker(t):
+        s = orc.SlotState.initial(U)
+        done, gen = 0, 0
+        while done < quota:
+            Dt = orc.build_target(7, s.x, s.x, s.x, seed=seed, gslot=t, gen=gen)
+            done += orc.batch_sample(U, s, Dt, t % 5, T=T, B=B, tabu=8, seed=seed, slot=t, gen=gen,
+                                     flip_limit=quota - done)
+            gen += 1
+        results[t] = done
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(cores)]
+    t0 = time.perf_counter()
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    dt = time.perf_counter() - t0
+    return sum(results), dt, cores, quota
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+        self.out = os.path.join("/tmp", f"dabs_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.out, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.out):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make(args.workload, seed=1)
+    per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(U, meta, per_step / 4, args.seed)
+    flips = 0
+    secs = 0.0
+    cores = quota = 0
+    for _ in range(args.steps):
+        f, dt, cores, quota = oracle_sample(U, meta, per_step, args.seed)
+        flips += f
+        secs += dt
+    value = flips / secs
+    sample = (f"{args.steps} steps x {cores} threads x {quota} flips of persistent slots from X=0 "
+              f"(random targets, algorithm = thread mod 5), workload {args.workload}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": config_of(args.workload, U, meta, None),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def config_of(workload, U, meta, solver):
+    n = int(U.shape[0])
+    c = {"workload": workload, "n": n, "s": meta["s_milli"] / 1000, "b": meta["b_milli"] / 1000,
+         "W_bytes": 2 * n * n}
+    if solver is not None:
+        c.update(slots_per_gpu=solver.slots, pools_per_gpu=solver.pools, threads_per_search=solver.threads,
+                 T=solver.T, B=solver.B)
+    c["l2"] = ("inputs larger than L2 (W streamed from HBM)" if 2 * n * n > L2_BYTES
+               else "L2 flushed (256 MiB write) between timed steps")
+    return c
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_2207_03069_b200 import Solver, build, torch_exchange
+    from paper_2207_03069_b200 import workloads as wl
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    U, meta = wl.make(args.workload, seed=1)
+    n = U.shape[0]
+    stream = torch.cuda.Stream()
+    solver = Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=meta.get("pools", 1),
+                    slots=meta.get("slots", 0), rank=rank, world=world, device=torch.cuda.current_device(),
+                    stream=stream.cuda_stream, exchange=torch_exchange() if world > 1 else None)
+    solver.reset(args.seed)
+    for _ in range(args.warmup):
+        solver.generation()
+    flush = None
+    if 2 * n * n <= L2_BYTES:
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    clocks = Clocks(torch.cuda.current_device())
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    st0 = solver.stats()
+    batch_ms = []
+    local_flips = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    prev_local = st0.local_flips
+    for k in range(args.steps):
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+        ev[k][0].record(stream)
+        solver.generation()
+        ev[k][1].record(stream)
+        s = solver.stats()
+        batch_ms.append(s.batch_ms_last)
+        local_flips.append(s.local_flips - prev_local)
+        prev_local = s.local_flips
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    st1 = solver.stats()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    flips = st1.total_flips - st0.total_flips
+    value = flips / (t_ms / 1e3)
+
+    # roofline of the dominant kernel (batch_kernel): algorithmic bytes = one
+    # W row (2n bytes, int16) per flip
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    avg_batch_ms = float(np.mean(batch_ms))
+    bytes_per_launch = float(np.mean(local_flips)) * 2 * n
+    achieved = bytes_per_launch / (avg_batch_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(args.workload, {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "kernel": "batch_kernel",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "bytes_per_flip": 2 * n, "batch_share_of_step": sum(batch_ms) / t_ms if world == 1 else None}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": config_of(args.workload, U, meta, solver), "roofline": roofline,
+        "gpu_launches": 5 * args.steps, "clocks": clk,
+        "per_gpu_flips_per_s": value / world,
+        "best_energy": st1.best_energy, "generations": int(st1.generations),
+    }
+    # ---- e2e: through the public API from pinned host memory, every step:
+    # dabs_create (H2D of W) + one generation (dabs_run with a one-generation
+    # budget) + D2H of the best vector and energy.
+    if not args.no_e2e:
+        Wp = torch.from_numpy(U).pin_memory()
+        Wnp = Wp.numpy()
+        e2e_flips, e2e_s = 0, 0.0
+        budget = max(1, int(np.mean(local_flips)) * world)
+        for k in range(max(1, min(args.steps, 3))):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s2 = Solver(Wnp, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=meta.get("pools", 1),
+                        slots=meta.get("slots", 0), rank=rank, world=world,
+                        device=torch.cuda.current_device(), stream=stream.cuda_stream,
+                        exchange=torch_exchange() if world > 1 else None)
+            E, x = s2.run(seed=args.seed + k, flip_budget=budget)
+            dt = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            e2e_flips += s2.stats().total_flips
+            e2e_s += dt
+            s2.close()
+        out["e2e"] = {"value": e2e_flips / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(2 * n * n),
+                      "d2h_bytes_per_step": int(n + 8), "steps": max(1, min(args.steps, 3)),
+                      "what": "dabs_create(W from pinned host) + dabs_run(one generation) + best readback"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        f, dt, cores, quota = oracle_sample(U, meta, args.cpu_seconds, args.seed)
+        out["cpu_baseline"] = {"value": f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+                               "sample": f"{cores} threads x {quota} flips, persistent slots from X=0 "
+                                         f"(random targets, algorithm = thread mod 5), {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(out))
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,7 @@ typedef struct {
     int64_t ebest;
     int64_t flips;    /* flips in this batch */
     int T, B;
+    int64_t flip_limit;   /* sampling bound for timing only (0 = none): stop after this many flips */
     /* randomness */
     uint64_t seed;
     uint32_t slot, gen;
@@ -197,6 +198,7 @@ static void flip(search_t* s, int i)
     }
     s->flips++;
     if (s->checked) check_state(s);
+    if (s->flip_limit && s->flips >= s->flip_limit && !s->err) s->err = 4;
 }
 
 /* Step 1 (typos read as R-2): minE over all 1-bit neighbours,     */
@@ -429,14 +431,35 @@ int orc_flip_factor(int milli, int n)
  * flip.  Returns 0, or an error code: 1/2 checked-mode mismatch, 3 empty
  * selection.
  */
+int orc_batch_limited(const int16_t* U, int n, int T, int B, int tabu,
+                      uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
+                      const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
+                      uint8_t* best, int64_t* ebest, int64_t* flips,
+                      int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked,
+                      int64_t flip_limit);
+
 int orc_batch(const int16_t* U, int n, int T, int B, int tabu,
               uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
               const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
               uint8_t* best, int64_t* ebest, int64_t* flips,
               int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked)
 {
+    return orc_batch_limited(U, n, T, B, tabu, x, delta, E, ring, D, algo, seed, slot, gen, best, ebest,
+                             flips, tr_bit, tr_E, tr_phase, tr_cap, checked, 0);
+}
+
+/* Same as orc_batch, but stops after flip_limit flips (returns 4): a bounded
+   sample of a batch, used only to time the oracle (bench cpu_baseline). */
+int orc_batch_limited(const int16_t* U, int n, int T, int B, int tabu,
+                      uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
+                      const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
+                      uint8_t* best, int64_t* ebest, int64_t* flips,
+                      int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked,
+                      int64_t flip_limit)
+{
     search_t s;
     memset(&s, 0, sizeof s);
+    s.flip_limit = flip_limit;
     s.n = n; s.U = U; s.x = x; s.delta = delta; s.E = *E; s.ring = ring; s.tabu = tabu;
     s.best = best; s.T = T; s.B = B; s.seed = seed; s.slot = slot; s.gen = gen;
     s.tr_bit = tr_bit; s.tr_E = tr_E; s.tr_phase = tr_phase; s.tr_cap = tr_cap;

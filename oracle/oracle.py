@@ -58,6 +58,8 @@ def lib():
                                 P, P, P,
                                 P, P, P, i64, C.c_int]
         L.orc_batch.restype = C.c_int
+        L.orc_batch_limited.argtypes = L.orc_batch.argtypes + [i64]
+        L.orc_batch_limited.restype = C.c_int
         L.orc_step_flip.argtypes = [P, C.c_int, P, P, P, P, C.c_int]
         L.orc_world_new.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     u32, u32, u32, C.c_int, C.c_int, C.c_int, C.c_int]
@@ -200,6 +202,26 @@ def batch(U: np.ndarray, state: SlotState, D: np.ndarray, algo: int, *, T: int, 
         m = min(f, trace_cap)
         tb, te, tp = tb[:m], te[:m], tp[:m]
     return BatchResult(best, int(ebest[0]), f, tb, te, tp)
+
+
+def batch_sample(U: np.ndarray, state: SlotState, D: np.ndarray, algo: int, *, T: int, B: int, tabu: int,
+                 seed: int, slot: int, gen: int, flip_limit: int) -> int:
+    """Run a batch but stop after ``flip_limit`` flips; returns the flips done.
+    Timing aid only (bench cpu_baseline); releases the GIL inside C."""
+    U = np.ascontiguousarray(U, dtype=np.int16)
+    n = U.shape[0]
+    D = np.ascontiguousarray(D, dtype=np.uint8)
+    best = np.zeros(n, np.uint8)
+    E = np.array([state.E], np.int64)
+    ebest = np.zeros(1, np.int64)
+    flips = np.zeros(1, np.int64)
+    err = lib().orc_batch_limited(_p(U), n, T, B, tabu, _p(state.x), _p(state.delta), _p(E), _p(state.ring),
+                                  _p(D), algo, seed, slot, gen, _p(best), _p(ebest), _p(flips),
+                                  None, None, None, 0, 0, flip_limit)
+    if err not in (0, 4):
+        raise RuntimeError(f"oracle batch error {err}")
+    state.E = int(E[0])
+    return int(flips[0])
 
 
 def step_flip(U: np.ndarray, state: SlotState, i: int) -> None:

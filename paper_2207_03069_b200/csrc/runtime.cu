@@ -1,0 +1,758 @@
+// runtime.cu -- the C ABI (include/dabs.h) over the sm_100a kernels.
+//
+// One context = one rank (one GPU): W, the slots (persistent searches), the
+// packets, P solution pools + the Xrossover successor snapshot, statistics,
+// and the exchange buffers.  A generation is GA seed -> batch -> merge ->
+// pack -> (exchange) -> import, all on one stream (R-25, R-26).
+// Citations: P:n = PAPER.md line n; R-x = DESIGN.md readings.
+#include <chrono>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dabs.h"
+#include "batch_kernel.cuh"
+#include "ga_pool_kernels.cuh"
+
+using namespace dabs;
+
+static thread_local std::string g_err;
+
+static dabs_status fail(dabs_status st, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(DABS_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,                \
+                        cudaGetErrorString(e_));                                              \
+    } while (0)
+
+struct dabs_ctx {
+    dabs_config cfg;
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // problem and tiling
+    int n = 0, n_pad = 0, nwp = 0, C = 0, NT = 0;
+    bool mw = false;
+    int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
+    GaConst ga{};
+    // device buffers
+    std::vector<void*> allocs;
+    int16_t* W = nullptr;
+    int32_t* diag = nullptr;
+    int32_t *wtab = nullptr, *ptab = nullptr;
+    uint32_t* X = nullptr;
+    int32_t* delta = nullptr;
+    int64_t* E = nullptr;
+    int32_t* ring = nullptr;
+    uint32_t* D = nullptr;
+    uint8_t *palgo = nullptr, *pgenop = nullptr;
+    uint32_t* best = nullptr;
+    int64_t *ebest = nullptr, *flips = nullptr;
+    PoolView* pools_d = nullptr;          // [P+1]
+    std::vector<PoolView> pools_h;        // host copy of the views
+    MergeArgs margs{};
+    unsigned long long* dispatch = nullptr;
+    unsigned long long* inserted = nullptr;
+    unsigned long long* flip_total = nullptr;   // this rank, cumulative
+    unsigned long long* scratch64 = nullptr;    // energy / checks
+    uint8_t* xbytes = nullptr;                  // energy input
+    PayloadLayout L{};
+    uint8_t *send = nullptr, *recv = nullptr;
+    // trace
+    int trace_slot = -1;
+    int64_t trace_cap = 0;
+    int32_t* tr_bit = nullptr;
+    int64_t* tr_E = nullptr;
+    int8_t* tr_phase = nullptr;
+    // run state (host)
+    bool ready = false;
+    uint64_t seed = 0;
+    uint32_t gen = 0;
+    uint64_t total_flips = 0, local_flips = 0;
+    int64_t best_E = E_INF;
+    std::vector<uint8_t> best_X;
+    int32_t rec[4] = {-1, -1, -1, -1};
+    uint64_t wall_ns = 0, ttb_ns = 0;
+    float batch_ms = 0, ga_ms = 0, merge_ms = 0;
+    cudaEvent_t ev[6] = {};
+    std::chrono::steady_clock::time_point t_reset;
+};
+
+template <typename Tp>
+static dabs_status dalloc(dabs_ctx* c, Tp** p, size_t count)
+{
+    size_t bytes = count * sizeof(Tp);
+    if (bytes == 0) bytes = 16;
+    void* q = nullptr;
+    if (c->cfg.alloc) {
+        q = c->cfg.alloc(c->cfg.user, bytes, c->stream);
+        if (!q) return fail(DABS_E_NOMEM, "alloc hook failed for %zu bytes", bytes);
+    } else {
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) return fail(DABS_E_NOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    }
+    c->allocs.push_back(q);
+    *p = reinterpret_cast<Tp*>(q);
+    return DABS_OK;
+}
+
+#define AL(ptr, count)                                         \
+    do {                                                       \
+        dabs_status st_ = dalloc(c, &(ptr), (size_t)(count));  \
+        if (st_ != DABS_OK) return st_;                        \
+    } while (0)
+
+extern "C" void dabs_config_default(dabs_config* cfg)
+{
+    if (!cfg) return;
+    memset(cfg, 0, sizeof *cfg);
+    cfg->struct_size = sizeof *cfg;
+    cfg->s_milli = 100;
+    cfg->b_milli = 1000;
+    cfg->tabu_period = 8;
+    cfg->pool_capacity = 100;
+    cfg->eps_ppm = 50000;
+    cfg->genop_mask = 0xFF;
+    cfg->algo_mask = 0x1F;
+    cfg->pools_per_gpu = 1;
+    cfg->slots_per_pool = 0;
+    cfg->target_energy = INT64_MIN;
+    cfg->time_limit_ns = 0;
+    cfg->rank = 0;
+    cfg->world = 1;
+    cfg->device = -1;
+}
+
+extern "C" const char* dabs_last_error(void) { return g_err.c_str(); }
+
+static int flip_factor(uint32_t milli, int n)
+{
+    const int64_t v = ((int64_t)milli * n + 999) / 1000;
+    return v < 1 ? 1 : (int)v;
+}
+
+// ---------------------------------------------------------------- kernels by tier
+using BatchFn = void (*)(const BatchParams);
+
+static BatchFn pick_batch(int C, bool mw, bool trace)
+{
+    if (mw) return trace ? batch_kernel<8, true, true> : batch_kernel<8, true, false>;
+    switch (C) {
+    case 1: return trace ? batch_kernel<1, false, true> : batch_kernel<1, false, false>;
+    case 2: return trace ? batch_kernel<2, false, true> : batch_kernel<2, false, false>;
+    case 4: return trace ? batch_kernel<4, false, true> : batch_kernel<4, false, false>;
+    default: return trace ? batch_kernel<8, false, true> : batch_kernel<8, false, false>;
+    }
+}
+
+static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
+{
+    BatchParams p{};
+    p.W = c->W; p.wtab = c->wtab; p.ptab = c->ptab;
+    p.n = c->n; p.n_pad = c->n_pad; p.nwp = c->nwp;
+    p.T = c->T; p.B = c->B; p.tabu = c->tabu;
+    p.seed = seed; p.gen = gen;
+    p.slot_base = (uint32_t)(c->cfg.rank * c->slots);
+    p.slot0 = slot0;
+    p.X = c->X; p.delta = c->delta; p.E = c->E; p.ring = c->ring;
+    p.D = c->D; p.algo = c->palgo;
+    p.best = c->best; p.ebest = c->ebest; p.flips = c->flips;
+    p.flip_total = c->flip_total;
+    p.trace_slot = c->trace_slot; p.tr_bit = c->tr_bit; p.tr_E = c->tr_E; p.tr_phase = c->tr_phase;
+    p.tr_cap = c->trace_cap;
+    return p;
+}
+
+// ---------------------------------------------------------------- create
+extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg_in,
+                                   dabs_ctx** out)
+{
+    if (!out) return fail(DABS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!W_host) return fail(DABS_E_ARG, "W is NULL");
+    if (n < 1 || n > 32768) return fail(DABS_E_ARG, "n=%d outside [1, 32768]", n);
+    dabs_config cfg;
+    dabs_config_default(&cfg);
+    if (cfg_in) {
+        if (cfg_in->struct_size != sizeof(dabs_config)) return fail(DABS_E_ARG, "dabs_config.struct_size mismatch");
+        cfg = *cfg_in;
+    }
+    if (cfg.tabu_period > 31) return fail(DABS_E_ARG, "tabu_period > 31");
+    if (cfg.pool_capacity < 1 || cfg.pool_capacity > 1024) return fail(DABS_E_ARG, "pool_capacity outside [1,1024]");
+    if (cfg.s_milli < 1 || cfg.b_milli < 1) return fail(DABS_E_ARG, "s and b must be positive");
+    if ((cfg.genop_mask & 0xFF) == 0 || (cfg.algo_mask & 0x1F) == 0) return fail(DABS_E_ARG, "empty genop/algo mask");
+    if (cfg.eps_ppm > 1000000) return fail(DABS_E_ARG, "eps_ppm > 1e6");
+    if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return fail(DABS_E_ARG, "bad rank/world");
+    if (cfg.world > 1 && !cfg.exchange) return fail(DABS_E_ARG, "world > 1 needs an exchange hook");
+    if (cfg.pools_per_gpu < 1) return fail(DABS_E_ARG, "pools_per_gpu < 1");
+
+    dabs_ctx* c = new dabs_ctx();
+    c->cfg = cfg;
+    auto bail = [&](dabs_status st) {
+        dabs_destroy(c);
+        return st;
+    };
+    int ndev = 0;
+    cudaError_t e0 = cudaGetDeviceCount(&ndev);
+    if (e0 != cudaSuccess || ndev == 0) {
+        fail(DABS_E_CUDA, "no CUDA device: %s", cudaGetErrorString(e0));
+        return bail(DABS_E_CUDA);
+    }
+    c->dev = cfg.device >= 0 ? cfg.device : 0;
+    if (cfg.device < 0) cudaGetDevice(&c->dev);
+    if (cudaSetDevice(c->dev) != cudaSuccess) {
+        fail(DABS_E_CUDA, "cudaSetDevice(%d) failed", c->dev);
+        return bail(DABS_E_CUDA);
+    }
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, c->dev);
+    if (prop.major != 10) {
+        fail(DABS_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", c->dev, prop.major, prop.minor);
+        return bail(DABS_E_CUDA);
+    }
+    if (cfg.cuda_stream) {
+        c->stream = (cudaStream_t)cfg.cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            fail(DABS_E_CUDA, "stream create failed");
+            return bail(DABS_E_CUDA);
+        }
+        c->own_stream = true;
+    }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+
+    // ---- tiling: warp per search for n <= 2048, else a CTA
+    c->n = n;
+    if (n <= 2048) {
+        c->mw = false;
+        c->NT = 32;
+        int C = 1;
+        while (C * 256 < n) C <<= 1;
+        c->C = C;
+    } else {
+        c->mw = true;
+        c->C = 8;
+        int NT = 64;
+        while (NT * 64 < n) NT <<= 1;
+        c->NT = NT;
+    }
+    c->n_pad = c->NT * c->C * 8;
+    c->nwp = c->n_pad / 32;
+    c->T = flip_factor(cfg.s_milli, n);
+    c->B = flip_factor(cfg.b_milli, n);
+    c->tabu = (int)cfg.tabu_period;
+    c->cap = (int)cfg.pool_capacity;
+    c->P = (int)cfg.pools_per_gpu;
+    if (cfg.slots_per_pool) {
+        c->S = (int)cfg.slots_per_pool;
+    } else {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->mw, false), c->NT, 0);
+        if (occ < 1) occ = 1;
+        const int conc = prop.multiProcessorCount * occ;
+        c->S = (2 * conc + c->P - 1) / c->P;   // about two waves per generation
+    }
+    c->slots = c->P * c->S;
+    if ((int64_t)c->slots * (cfg.world) >= (1ll << 31)) return bail(fail(DABS_E_ARG, "too many slots"));
+
+    // ---- GA constants
+    GaConst& g = c->ga;
+    g.n = n; g.nwp = c->nwp; g.cap = c->cap; g.P = c->P; g.S = c->S;
+    g.eps_thr = (uint32_t)(((uint64_t)cfg.eps_ppm << 32) / 1000000u);
+    g.n_gen = 0; g.n_alg = 0;
+    for (int k = 0; k < N_GEN; k++) if (cfg.genop_mask >> k & 1) g.gens[g.n_gen++] = k;
+    for (int k = 0; k < N_ALG; k++) if (cfg.algo_mask >> k & 1) g.algs[g.n_alg++] = k;
+
+    // ---- a1: upload, check, symmetrize
+    int16_t* U = nullptr;
+    dabs_status st;
+    if ((st = dalloc(c, &U, (size_t)n * n)) != DABS_OK) return bail(st);
+    if ((st = dalloc(c, &c->scratch64, 4)) != DABS_OK) return bail(st);
+    if (cudaMemcpyAsync(U, W_host, sizeof(int16_t) * (size_t)n * n, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->scratch64, 0, 32, c->stream) != cudaSuccess)
+        return bail(fail(DABS_E_CUDA, "upload of W failed"));
+    check_kernel<<<n, 256, 0, c->stream>>>(U, n, c->scratch64);
+    unsigned long long flags[2];
+    if (cudaMemcpyAsync(flags, c->scratch64, 16, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return bail(fail(DABS_E_CUDA, "check kernel failed: %s", cudaGetErrorString(cudaGetLastError())));
+    if (flags[0]) return bail(fail(DABS_E_TRIANGLE, "W has a nonzero entry below the diagonal"));
+    if (flags[1] >= (unsigned long long)INT32_MAX)
+        return bail(fail(DABS_E_RANGE, "max_k sum_j |W_kj| = %llu does not fit int32 Delta", flags[1]));
+    if ((st = dalloc(c, &c->W, (size_t)n * c->n_pad)) != DABS_OK) return bail(st);
+    if ((st = dalloc(c, &c->diag, c->n_pad)) != DABS_OK) return bail(st);
+    if (cudaMemsetAsync(c->W, 0, sizeof(int16_t) * (size_t)n * c->n_pad, c->stream) != cudaSuccess)
+        return bail(fail(DABS_E_CUDA, "memset W"));
+    {
+        dim3 grid((c->n_pad + 31) / 32, (n + 31) / 32), blk(32, 8);
+        symmetrize_kernel<<<grid, blk, 0, c->stream>>>(U, n, c->n_pad, c->W, c->diag);
+    }
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return bail(fail(DABS_E_CUDA, "symmetrize: %s", cudaGetErrorString(cudaGetLastError())));
+    // free the staging copy
+    for (auto it = c->allocs.begin(); it != c->allocs.end(); ++it)
+        if (*it == U) {
+            if (c->cfg.free) c->cfg.free(c->cfg.user, U, c->stream); else cudaFree(U);
+            c->allocs.erase(it);
+            break;
+        }
+
+    // ---- schedule tables for CyclicMin (R-7) and RandomMin (R-8)
+    {
+        std::vector<int32_t> wt(c->T + 1), pt(c->T + 1);
+        const unsigned __int128 T3 = (unsigned __int128)c->T * c->T * c->T;
+        for (int t = 0; t <= c->T; t++) {
+            const unsigned __int128 t3 = (unsigned __int128)t * t * t;
+            uint64_t w = (uint64_t)(((unsigned __int128)n * t3 + T3 - 1) / T3);
+            const uint64_t cmin = n < 32 ? (uint64_t)n : 32u;
+            if (w < cmin) w = cmin;
+            if (w > (uint64_t)n) w = n;
+            wt[t] = (int32_t)w;
+            uint64_t p = (uint64_t)(((unsigned __int128)65536u * t3) / T3);
+            const uint64_t pf = 2097152u / (uint32_t)n;
+            if (p < pf) p = pf;
+            if (p > 65536u) p = 65536u;
+            pt[t] = (int32_t)p;
+        }
+        if ((st = dalloc(c, &c->wtab, c->T + 1)) != DABS_OK) return bail(st);
+        if ((st = dalloc(c, &c->ptab, c->T + 1)) != DABS_OK) return bail(st);
+        cudaMemcpyAsync(c->wtab, wt.data(), 4 * wt.size(), cudaMemcpyHostToDevice, c->stream);
+        cudaMemcpyAsync(c->ptab, pt.data(), 4 * pt.size(), cudaMemcpyHostToDevice, c->stream);
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DABS_E_CUDA, "tables"));
+    }
+
+    // ---- slots, packets, pools
+    const size_t ns = c->slots, nwp = c->nwp, cap = c->cap, P = c->P;
+#define AB(ptr, count) if ((st = dalloc(c, &(ptr), (count))) != DABS_OK) return bail(st)
+    AB(c->X, ns * nwp); AB(c->delta, ns * c->n_pad); AB(c->E, ns); AB(c->ring, ns * TABU_RING);
+    AB(c->D, ns * nwp); AB(c->palgo, ns); AB(c->pgenop, ns);
+    AB(c->best, ns * nwp); AB(c->ebest, ns); AB(c->flips, ns);
+    AB(c->dispatch, P * N_ALG * N_GEN); AB(c->inserted, P * N_ALG * N_GEN);
+    AB(c->flip_total, 1); AB(c->xbytes, (size_t)n);
+    c->pools_h.resize(P + 1);
+    for (size_t q = 0; q <= P; q++) {
+        PoolView& v = c->pools_h[q];
+        AB(v.X, cap * nwp); AB(v.E, cap); AB(v.seq, cap); AB(v.algo, cap); AB(v.genop, cap);
+    }
+    AB(c->pools_d, P + 1);
+    cudaMemcpyAsync(c->pools_d, c->pools_h.data(), sizeof(PoolView) * (P + 1), cudaMemcpyHostToDevice, c->stream);
+    MergeArgs& m = c->margs;
+    m.pools = c->pools_d; m.best = c->best; m.ebest = c->ebest; m.palgo = c->palgo; m.pgenop = c->pgenop;
+    AB(m.order, ns); AB(m.acc, P * cap); AB(m.sX, P * cap * nwp); AB(m.sE, P * cap); AB(m.sSeq, P * cap);
+    AB(m.sAlgo, P * cap); AB(m.sGenop, P * cap);
+    m.inserted = c->inserted;
+    m.slot_base = (uint32_t)(cfg.rank * c->slots);
+    m.S = c->S; m.cap = c->cap; m.nwp = c->nwp;
+    // payload layout (8-byte aligned fields)
+    {
+        PayloadLayout& L = c->L;
+        size_t o = 0;
+        auto al8 = [](size_t v) { return (v + 7) & ~(size_t)7; };
+        L.oX = o; o = al8(o + 4 * cap * nwp);
+        L.oE = o; o = al8(o + 8 * cap);
+        L.oSeq = o; o = al8(o + 8 * cap);
+        L.oAlgo = o; o = al8(o + cap);
+        L.oGenop = o; o = al8(o + cap);
+        L.oSum = o; o = al8(o + sizeof(Summary));
+        L.oBestX = o; o = al8(o + 4 * nwp);
+        L.bytes = o;
+    }
+    AB(c->send, c->L.bytes);
+    AB(c->recv, c->L.bytes * (size_t)cfg.world);
+#undef AB
+    c->best_X.assign(n, 0);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DABS_E_CUDA, "create: %s", cudaGetErrorString(cudaGetLastError())));
+    *out = c;
+    return DABS_OK;
+}
+
+extern "C" void dabs_destroy(dabs_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* q : c->allocs) {
+        if (c->cfg.free) c->cfg.free(c->cfg.user, q, c->stream); else cudaFree(q);
+    }
+    for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+// ---------------------------------------------------------------- reset / generation
+extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    CK(cudaSetDevice(c->dev));
+    c->seed = seed;
+    c->ga.seed = seed;
+    c->gen = 0;
+    init_slots_kernel<<<c->slots, 256, 0, c->stream>>>(c->slots, c->n_pad, c->nwp, c->diag, c->X, c->delta,
+                                                       c->E, c->ring);
+    const uint32_t gid0 = (uint32_t)(c->cfg.rank * c->P);
+    const uint32_t nbr_gid = (uint32_t)(((c->cfg.rank + 1) * c->P) % (c->cfg.world * c->P));
+    init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, c->stream>>>(c->ga, c->pools_d, gid0, nbr_gid);
+    CK(cudaMemsetAsync(c->dispatch, 0, 8 * c->P * N_ALG * N_GEN, c->stream));
+    CK(cudaMemsetAsync(c->inserted, 0, 8 * c->P * N_ALG * N_GEN, c->stream));
+    CK(cudaMemsetAsync(c->flip_total, 0, 8, c->stream));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    c->total_flips = 0;
+    c->local_flips = 0;
+    c->best_E = E_INF;
+    std::fill(c->best_X.begin(), c->best_X.end(), 0);
+    c->rec[0] = c->rec[1] = c->rec[2] = c->rec[3] = -1;
+    c->wall_ns = 0;
+    c->ttb_ns = 0;
+    c->t_reset = std::chrono::steady_clock::now();
+    c->ready = true;
+    return DABS_OK;
+}
+
+static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0, int count, bool trace)
+{
+    BatchParams p = batch_params(c, seed, gen, slot0);
+    BatchFn fn = pick_batch(c->C, c->mw, trace);
+    fn<<<count, c->NT, 0, c->stream>>>(p);
+    CK(cudaGetLastError());
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_generation(dabs_ctx* c)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    if (!c->ready) return fail(DABS_E_STATE, "dabs_generation before dabs_reset");
+    CK(cudaSetDevice(c->dev));
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
+    // a3: GA seeding
+    CK(cudaEventRecord(c->ev[0], st));
+    ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, st>>>(c->ga, c->pools_d, (uint32_t)(c->cfg.rank * c->slots),
+                                                        c->gen, c->slots, c->D, c->palgo, c->pgenop,
+                                                        c->dispatch);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[1], st));
+    // a4-a7: one batch search per slot (the hot loop)
+    dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0);
+    if (s1 != DABS_OK) return s1;
+    CK(cudaEventRecord(c->ev[2], st));
+    // a8: pool merge
+    c->margs.gen = c->gen;
+    pool_merge_kernel<<<c->P, 1024, 0, st>>>(c->margs);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[3], st));
+    // a9: exchange
+    pack_payload_kernel<<<1, 256, 0, st>>>(c->pools_d, c->P, c->cap, c->nwp, (uint32_t)(c->cfg.rank * c->P),
+                                           c->flip_total, c->send, c->L);
+    CK(cudaGetLastError());
+    const uint8_t* gathered = c->send;
+    if (c->cfg.world > 1) {
+        const int rc = c->cfg.exchange(c->cfg.user, c->send, c->recv, c->L.bytes, st);
+        if (rc != 0) return fail(DABS_E_COMM, "exchange hook returned %d", rc);
+        gathered = c->recv;
+    }
+    const int succ_rank = (c->cfg.rank + 1) % c->cfg.world;
+    import_snapshot_kernel<<<8, 256, 0, st>>>(gathered + (size_t)succ_rank * c->L.bytes, c->pools_h[c->P],
+                                              c->cap, c->nwp, c->L);
+    CK(cudaGetLastError());
+    // summaries of all ranks to the host
+    std::vector<Summary> sums(c->cfg.world);
+    for (int r = 0; r < c->cfg.world; r++)
+        CK(cudaMemcpyAsync(&sums[r], gathered + (size_t)r * c->L.bytes + c->L.oSum, sizeof(Summary),
+                           cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaEventElapsedTime(&c->ga_ms, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&c->merge_ms, c->ev[2], c->ev[3]);
+    uint64_t tot = 0;
+    int br = 0;
+    for (int r = 0; r < c->cfg.world; r++) {
+        tot += sums[r].flips;
+        if (sums[r].bestE < sums[br].bestE) br = r;
+    }
+    c->total_flips = tot;
+    c->local_flips = sums[c->cfg.rank].flips;
+    const auto t1 = std::chrono::steady_clock::now();
+    c->wall_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    if (sums[br].bestE < c->best_E) {
+        c->best_E = sums[br].bestE;
+        std::vector<uint32_t> words(c->nwp);
+        CK(cudaMemcpy(words.data(), gathered + (size_t)br * c->L.bytes + c->L.oBestX, 4 * c->nwp,
+                      cudaMemcpyDeviceToHost));
+        for (int k = 0; k < c->n; k++) c->best_X[k] = (uint8_t)((words[k >> 5] >> (k & 31)) & 1u);
+        c->rec[0] = sums[br].algo;
+        c->rec[1] = sums[br].genop;
+        c->rec[2] = (int32_t)((sums[br].bestSeq >> 32) - 1);
+        c->rec[3] = (int32_t)(sums[br].bestSeq & 0xFFFFFFFFu);
+        c->ttb_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - c->t_reset).count();
+    }
+    c->gen++;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_run(dabs_ctx* c, uint64_t seed, uint64_t flip_budget, uint8_t* best_x,
+                                int64_t* best_e)
+{
+    dabs_status st = dabs_reset(c, seed);
+    if (st != DABS_OK) return st;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        st = dabs_generation(c);
+        if (st != DABS_OK) return st;
+        if (c->total_flips >= flip_budget) break;
+        if (c->cfg.target_energy != INT64_MIN && c->best_E <= c->cfg.target_energy) break;
+        if (c->cfg.time_limit_ns) {
+            const auto ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+            if ((uint64_t)ns >= c->cfg.time_limit_ns) break;
+        }
+    }
+    return dabs_best(c, best_x, best_e);
+}
+
+extern "C" dabs_status dabs_best(const dabs_ctx* c, uint8_t* best_x, int64_t* best_e)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    if (best_x) memcpy(best_x, c->best_X.data(), c->n);
+    if (best_e) *best_e = c->best_E;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_energy(const dabs_ctx* cc, const uint8_t* x, int64_t* e)
+{
+    dabs_ctx* c = const_cast<dabs_ctx*>(cc);
+    if (!c || !x || !e) return fail(DABS_E_ARG, "NULL argument");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaMemcpyAsync(c->xbytes, x, c->n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->scratch64, 0, 8, c->stream));
+    energy_kernel<<<c->n, 256, 0, c->stream>>>(c->W, c->diag, c->n, c->n_pad, c->xbytes, (long long*)c->scratch64);
+    CK(cudaGetLastError());
+    long long v = 0;
+    CK(cudaMemcpyAsync(&v, c->scratch64, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *e = v;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
+{
+    if (!c || !o) return fail(DABS_E_ARG, "NULL argument");
+    memset(o, 0, sizeof *o);
+    o->total_flips = c->total_flips;
+    o->local_flips = c->local_flips;
+    o->generations = c->gen;
+    o->wall_ns = c->wall_ns;
+    o->time_to_best_ns = c->ttb_ns;
+    o->batch_ms_last = c->batch_ms;
+    o->ga_ms_last = c->ga_ms;
+    o->merge_ms_last = c->merge_ms;
+    o->best_energy = c->best_E;
+    o->best_algo = c->rec[0]; o->best_genop = c->rec[1]; o->best_generation = c->rec[2]; o->best_slot = c->rec[3];
+    std::vector<unsigned long long> d(c->P * N_ALG * N_GEN), in(c->P * N_ALG * N_GEN);
+    if (cudaMemcpy(d.data(), c->dispatch, 8 * d.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(in.data(), c->inserted, 8 * in.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(DABS_E_CUDA, "stats copy failed");
+    for (int p = 0; p < c->P; p++)
+        for (int a = 0; a < N_ALG; a++)
+            for (int g = 0; g < N_GEN; g++) {
+                o->dispatch[a][g] += d[(p * N_ALG + a) * N_GEN + g];
+                o->inserted[a][g] += in[(p * N_ALG + a) * N_GEN + g];
+            }
+    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = c->NT; o->slots = c->slots; o->pools = c->P;
+    o->T = c->T; o->B = c->B; o->cap = c->cap;
+    return DABS_OK;
+}
+
+// ---------------------------------------------------------------- parity hooks
+static void bytes_to_words(const uint8_t* x, int n, std::vector<uint32_t>& w)
+{
+    std::fill(w.begin(), w.end(), 0u);
+    for (int k = 0; k < n; k++) if (x[k]) w[k >> 5] |= 1u << (k & 31);
+}
+static void words_to_bytes(const std::vector<uint32_t>& w, int n, uint8_t* x)
+{
+    for (int k = 0; k < n; k++) x[k] = (uint8_t)((w[k >> 5] >> (k & 31)) & 1u);
+}
+
+static dabs_status ensure_trace(dabs_ctx* c, int64_t cap)
+{
+    if (cap <= c->trace_cap && c->tr_bit) return DABS_OK;
+    dabs_status st;
+    if ((st = dalloc(c, &c->tr_bit, cap)) != DABS_OK) return st;
+    if ((st = dalloc(c, &c->tr_E, cap)) != DABS_OK) return st;
+    if ((st = dalloc(c, &c->tr_phase, cap)) != DABS_OK) return st;
+    c->trace_cap = cap;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_debug_batch(dabs_ctx* c, uint32_t slot, uint8_t* x, int32_t* delta, int64_t* E,
+                                        int32_t* ring, const uint8_t* D, int32_t algo, uint64_t seed,
+                                        uint32_t gen, uint8_t* best, int64_t* ebest, int64_t* flips,
+                                        int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t trace_cap)
+{
+    if (!c || !x || !delta || !E || !ring || !D || !best || !ebest || !flips) return fail(DABS_E_ARG, "NULL argument");
+    if (slot >= (uint32_t)c->slots) return fail(DABS_E_ARG, "slot out of range");
+    if (algo < 0 || algo >= N_ALG) return fail(DABS_E_ARG, "algo out of range");
+    CK(cudaSetDevice(c->dev));
+    const int n = c->n;
+    std::vector<uint32_t> w(c->nwp);
+    bytes_to_words(x, n, w);
+    CK(cudaMemcpy(c->X + (size_t)slot * c->nwp, w.data(), 4 * c->nwp, cudaMemcpyHostToDevice));
+    bytes_to_words(D, n, w);
+    CK(cudaMemcpy(c->D + (size_t)slot * c->nwp, w.data(), 4 * c->nwp, cudaMemcpyHostToDevice));
+    std::vector<int32_t> dp(c->n_pad, INT32_MAX);
+    memcpy(dp.data(), delta, 4 * (size_t)n);
+    CK(cudaMemcpy(c->delta + (size_t)slot * c->n_pad, dp.data(), 4 * (size_t)c->n_pad, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->E + slot, E, 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->ring + (size_t)slot * TABU_RING, ring, 4 * TABU_RING, cudaMemcpyHostToDevice));
+    const uint8_t a8 = (uint8_t)algo;
+    CK(cudaMemcpy(c->palgo + slot, &a8, 1, cudaMemcpyHostToDevice));
+    const int64_t tcap = trace_cap > 0 ? trace_cap : 1;
+    dabs_status st = ensure_trace(c, tcap);
+    if (st != DABS_OK) return st;
+    const int saved_slot = c->trace_slot;
+    const int64_t saved_cap = c->trace_cap;
+    c->trace_slot = (int)slot;
+    c->trace_cap = trace_cap > 0 ? trace_cap : 0;
+    st = launch_batch(c, seed, gen, (int)slot, 1, true);
+    c->trace_slot = saved_slot;
+    c->trace_cap = saved_cap;
+    if (st != DABS_OK) return st;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(w.data(), c->X + (size_t)slot * c->nwp, 4 * c->nwp, cudaMemcpyDeviceToHost));
+    words_to_bytes(w, n, x);
+    CK(cudaMemcpy(dp.data(), c->delta + (size_t)slot * c->n_pad, 4 * (size_t)c->n_pad, cudaMemcpyDeviceToHost));
+    memcpy(delta, dp.data(), 4 * (size_t)n);
+    CK(cudaMemcpy(E, c->E + slot, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ring, c->ring + (size_t)slot * TABU_RING, 4 * TABU_RING, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(w.data(), c->best + (size_t)slot * c->nwp, 4 * c->nwp, cudaMemcpyDeviceToHost));
+    words_to_bytes(w, n, best);
+    CK(cudaMemcpy(ebest, c->ebest + slot, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flips, c->flips + slot, 8, cudaMemcpyDeviceToHost));
+    if (trace_cap > 0 && tr_bit && tr_E && tr_phase) {
+        const int64_t m = *flips < trace_cap ? *flips : trace_cap;
+        CK(cudaMemcpy(tr_bit, c->tr_bit, 4 * m, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tr_E, c->tr_E, 8 * m, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tr_phase, c->tr_phase, m, cudaMemcpyDeviceToHost));
+    }
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_read_slot(const dabs_ctx* c, uint32_t slot, uint8_t* x, int32_t* delta, int64_t* E,
+                                      int32_t* ring)
+{
+    if (!c || slot >= (uint32_t)c->slots) return fail(DABS_E_ARG, "bad ctx/slot");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<uint32_t> w(c->nwp);
+    if (x) {
+        CK(cudaMemcpy(w.data(), c->X + (size_t)slot * c->nwp, 4 * c->nwp, cudaMemcpyDeviceToHost));
+        words_to_bytes(w, c->n, x);
+    }
+    if (delta) CK(cudaMemcpy(delta, c->delta + (size_t)slot * c->n_pad, 4 * (size_t)c->n, cudaMemcpyDeviceToHost));
+    if (E) CK(cudaMemcpy(E, c->E + slot, 8, cudaMemcpyDeviceToHost));
+    if (ring) CK(cudaMemcpy(ring, c->ring + (size_t)slot * TABU_RING, 4 * TABU_RING, cudaMemcpyDeviceToHost));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_read_pool(const dabs_ctx* c, uint32_t pool, uint8_t* X, int64_t* E, uint64_t* seq,
+                                      uint8_t* algo, uint8_t* genop)
+{
+    if (!c || pool > (uint32_t)c->P) return fail(DABS_E_ARG, "bad ctx/pool");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    const PoolView& v = c->pools_h[pool];
+    if (X) {
+        std::vector<uint32_t> w((size_t)c->cap * c->nwp);
+        CK(cudaMemcpy(w.data(), v.X, 4 * w.size(), cudaMemcpyDeviceToHost));
+        for (int r = 0; r < c->cap; r++)
+            for (int k = 0; k < c->n; k++)
+                X[(size_t)r * c->n + k] = (uint8_t)((w[(size_t)r * c->nwp + (k >> 5)] >> (k & 31)) & 1u);
+    }
+    if (E) CK(cudaMemcpy(E, v.E, 8 * c->cap, cudaMemcpyDeviceToHost));
+    if (seq) CK(cudaMemcpy(seq, v.seq, 8 * c->cap, cudaMemcpyDeviceToHost));
+    if (algo) CK(cudaMemcpy(algo, v.algo, c->cap, cudaMemcpyDeviceToHost));
+    if (genop) CK(cudaMemcpy(genop, v.genop, c->cap, cudaMemcpyDeviceToHost));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_read_packet(const dabs_ctx* c, uint32_t slot, uint8_t* D, int32_t* algo,
+                                        int32_t* genop, uint8_t* best, int64_t* ebest, int64_t* flips)
+{
+    if (!c || slot >= (uint32_t)c->slots) return fail(DABS_E_ARG, "bad ctx/slot");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<uint32_t> w(c->nwp);
+    if (D) {
+        CK(cudaMemcpy(w.data(), c->D + (size_t)slot * c->nwp, 4 * c->nwp, cudaMemcpyDeviceToHost));
+        words_to_bytes(w, c->n, D);
+    }
+    if (best) {
+        CK(cudaMemcpy(w.data(), c->best + (size_t)slot * c->nwp, 4 * c->nwp, cudaMemcpyDeviceToHost));
+        words_to_bytes(w, c->n, best);
+    }
+    uint8_t a = 0, g = 0;
+    CK(cudaMemcpy(&a, c->palgo + slot, 1, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&g, c->pgenop + slot, 1, cudaMemcpyDeviceToHost));
+    if (algo) *algo = a;
+    if (genop) *genop = g;
+    if (ebest) CK(cudaMemcpy(ebest, c->ebest + slot, 8, cudaMemcpyDeviceToHost));
+    if (flips) CK(cudaMemcpy(flips, c->flips + slot, 8, cudaMemcpyDeviceToHost));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_read_stats_pool(const dabs_ctx* c, uint32_t pool, uint64_t* dispatch, uint64_t* inserted)
+{
+    if (!c || pool >= (uint32_t)c->P) return fail(DABS_E_ARG, "bad ctx/pool");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    const size_t off = (size_t)pool * N_ALG * N_GEN;
+    if (dispatch) CK(cudaMemcpy(dispatch, c->dispatch + off, 8 * N_ALG * N_GEN, cudaMemcpyDeviceToHost));
+    if (inserted) CK(cudaMemcpy(inserted, c->inserted + off, 8 * N_ALG * N_GEN, cudaMemcpyDeviceToHost));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_trace_enable(dabs_ctx* c, int32_t slot, int64_t cap)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    if (slot >= c->slots) return fail(DABS_E_ARG, "slot out of range");
+    if (slot < 0 || cap <= 0) {
+        c->trace_slot = -1;
+        return DABS_OK;
+    }
+    dabs_status st = ensure_trace(c, cap);
+    if (st != DABS_OK) return st;
+    c->trace_slot = slot;
+    c->trace_cap = cap;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_trace_read(const dabs_ctx* c, int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase,
+                                       int64_t* count)
+{
+    if (!c || c->trace_slot < 0) return fail(DABS_E_STATE, "tracing not enabled");
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t f = 0;
+    CK(cudaMemcpy(&f, c->flips + c->trace_slot, 8, cudaMemcpyDeviceToHost));
+    const int64_t m = f < c->trace_cap ? f : c->trace_cap;
+    if (tr_bit) CK(cudaMemcpy(tr_bit, c->tr_bit, 4 * m, cudaMemcpyDeviceToHost));
+    if (tr_E) CK(cudaMemcpy(tr_E, c->tr_E, 8 * m, cudaMemcpyDeviceToHost));
+    if (tr_phase) CK(cudaMemcpy(tr_phase, c->tr_phase, m, cudaMemcpyDeviceToHost));
+    if (count) *count = m;
+    return DABS_OK;
+}

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element, on the same seeded inputs.  All arithmetic is integer, so the bar is
+bit-exact: per-flip bit, E and phase; final X, Delta, E, tabu ring; BEST,
+E(BEST), flip count; pools, packets and statistics per generation.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ALGS = range(5)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2207_03069_b200 import build, dabs
+    build.build()
+    return dabs
+
+
+def rand_upper(rng, n, lo, hi):
+    U = rng.integers(lo, hi + 1, size=(n, n)).astype(np.int16)
+    return np.triu(U)
+
+
+def random_state(orc, rng, U, n_ring):
+    n = U.shape[0]
+    st = orc.SlotState.initial(U)
+    st.x[:] = rng.integers(0, 2, n)
+    st.delta[:] = orc.delta_closed(U, st.x)
+    st.E = orc.energy(U, st.x)
+    ring = np.full(32, -1, np.int32)
+    k = min(n_ring, 32)
+    ring[:k] = rng.integers(0, n, k)
+    st.ring[:] = ring
+    return st
+
+
+def compare_batch(orc, solver, U, st, D, algo, seed, gslot, gen, T, B, tabu):
+    n = U.shape[0]
+    cap = 4 * (B + 2 * n + 4 * n) + 1000
+    st_gpu = st.copy()
+    ref = orc.batch(U, st, D, algo, T=T, B=B, tabu=tabu, seed=seed, slot=gslot, gen=gen, trace_cap=cap)
+    got = solver.debug_batch(gslot - 0, st_gpu.x, st_gpu.delta, st_gpu.E, st_gpu.ring, D, algo, seed, gen,
+                             trace_cap=cap)
+    tag = f"n={n} algo={algo} seed={seed}"
+    assert got["flips"] == ref.flips, tag
+    m = min(ref.flips, cap)
+    np.testing.assert_array_equal(got["trace_bit"][:m], ref.trace_bit[:m], err_msg=tag)
+    np.testing.assert_array_equal(got["trace_E"][:m], ref.trace_E[:m], err_msg=tag)
+    np.testing.assert_array_equal(got["trace_phase"][:m], ref.trace_phase[:m], err_msg=tag)
+    np.testing.assert_array_equal(got["x"], st.x, err_msg=tag)
+    np.testing.assert_array_equal(got["delta"], st.delta, err_msg=tag)
+    assert got["E"] == st.E, tag
+    np.testing.assert_array_equal(got["ring"], st.ring, err_msg=tag)
+    assert got["ebest"] == ref.ebest, tag
+    np.testing.assert_array_equal(got["best"], ref.best, err_msg=tag)
+
+
+# sizes spanning every tier and ragged tails: warp tier C=1,2,4,8 and the CTA tier
+SIZES = [1, 2, 7, 16, 33, 255, 256, 257, 700, 1024, 1500, 2048, 2049, 5000, 9000]
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_batch_parity(orc, lib, n):
+    rng = np.random.default_rng(1000 + n)
+    lo, hi = (-32767, 32767) if n <= 32768 // 2 else (-100, 100)
+    if n > 2048:
+        lo, hi = -3000, 3000
+    U = rand_upper(rng, n, lo, hi)
+    s_milli, b_milli, tabu = 150, 1500, 8
+    solver = lib.Solver(U, s_milli=s_milli, b_milli=b_milli, tabu=tabu, pools=1, slots=2)
+    T, B = solver.T, solver.B
+    assert (T, B) == (orc.flip_factor(s_milli, n), orc.flip_factor(b_milli, n))
+    for algo in ALGS:
+        for rep in range(2):
+            st = random_state(orc, rng, U, n_ring=rep * 5)
+            D = rng.integers(0, 2, n).astype(np.uint8)
+            seed = int(rng.integers(0, 2**63))
+            compare_batch(orc, solver, U, st, D, algo, seed, gslot=1, gen=int(rng.integers(0, 1000)),
+                          T=T, B=B, tabu=tabu)
+    solver.close()
+
+
+@pytest.mark.parametrize("n", [16, 200])
+def test_batch_parity_structured(orc, lib, n):
+    """MaxCut-shaped (+-1, many ties) and zero-plateau instances stress the
+    lowest-index tie rules and the PositiveMin/MaxMin candidate counting."""
+    from paper_2207_03069_b200 import workloads as wl
+    rng = np.random.default_rng(n)
+    U, _, _ = wl.complete_pm1(n, seed=n)
+    solver = lib.Solver(U, s_milli=100, b_milli=3000, pools=1, slots=1)
+    for algo in ALGS:
+        st = random_state(orc, rng, U, n_ring=0)
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        compare_batch(orc, solver, U, st, D, algo, 77, 0, 3, solver.T, solver.B, 8)
+    # zero-diagonal, sparse: many Delta = 0
+    U = np.zeros((n, n), np.int16)
+    idx = rng.integers(0, n, size=(n, 2))
+    for a, b in idx:
+        if a != b:
+            U[min(a, b), max(a, b)] = rng.choice([-1, 1])
+    solver = lib.Solver(U, s_milli=100, b_milli=3000, pools=1, slots=1, tabu=3)
+    for algo in ALGS:
+        st = random_state(orc, rng, U, n_ring=2)
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        compare_batch(orc, solver, U, st, D, algo, 5, 0, 1, solver.T, solver.B, 3)
+
+
+def test_energy_parity(orc, lib):
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 300, 2049):
+        U = rand_upper(rng, n, -32767, 32767) if n < 1000 else rand_upper(rng, n, -100, 100)
+        solver = lib.Solver(U, pools=1, slots=1)
+        for _ in range(5):
+            x = rng.integers(0, 2, n).astype(np.uint8)
+            assert solver.energy(x) == orc.energy(U, x)
+        solver.close()
+
+
+def test_create_errors(lib):
+    U = np.zeros((4, 4), np.int16)
+    U[2, 1] = 1
+    with pytest.raises(lib.DabsError, match="E_TRIANGLE"):
+        lib.Solver(U)
+    with pytest.raises(lib.DabsError, match="E_ARG"):
+        lib.Solver(np.zeros((0, 0), np.int16))
+    with pytest.raises(lib.DabsError, match="E_ARG"):
+        lib.Solver(np.zeros((4, 4), np.int16), tabu=40)
+    # int16 weights with n <= 32768 can never overflow int32 Delta
+    # (32768 * 32767 < 2^31 - 1), so DABS_E_RANGE is a defensive check only.
+
+
+def compare_world(orc, solver, ow, P, gens_done):
+    for p in range(P + 1):
+        g = solver.read_pool(p)
+        r = ow.pool(p)
+        for k in ("E", "seq", "algo", "genop"):
+            np.testing.assert_array_equal(g[k], r[k], err_msg=f"pool {p} {k} gen {gens_done}")
+        np.testing.assert_array_equal(g["X"], r["X"], err_msg=f"pool {p} X gen {gens_done}")
+    for s in range(solver.slots):
+        g = solver.read_slot(s)
+        r = ow.slot(s)
+        np.testing.assert_array_equal(g["x"], r.x)
+        np.testing.assert_array_equal(g["delta"], r.delta)
+        assert g["E"] == r.E
+        np.testing.assert_array_equal(g["ring"], r.ring)
+        if gens_done == 0:
+            continue
+        gp = solver.read_packet(s)
+        rp = ow.packet(s)
+        for k in ("algo", "genop", "ebest", "flips"):
+            assert gp[k] == rp[k], (s, k)
+        np.testing.assert_array_equal(gp["D"], rp["D"])
+        np.testing.assert_array_equal(gp["best"], rp["best"])
+    d_ref, i_ref = ow.stats()
+    for p in range(P):
+        d, i = solver.read_stats_pool(p)
+        np.testing.assert_array_equal(d, d_ref[p])
+        np.testing.assert_array_equal(i, i_ref[p])
+
+
+@pytest.mark.parametrize("n,P,S,gens", [(40, 2, 7, 6), (300, 3, 5, 4), (2100, 2, 3, 2)])
+def test_generation_parity(orc, lib, n, P, S, gens):
+    rng = np.random.default_rng(n)
+    U = rand_upper(rng, n, -200, 200)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=S, cap=20)
+    sysm = orc.System(U, cfg, world=1)
+    solver = lib.Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=20)
+    seed = 12345
+    sysm.reset(seed)
+    solver.reset(seed)
+    compare_world(orc, solver, sysm.ranks[0], P, 0)
+    for g in range(gens):
+        sysm.generation()
+        solver.generation()
+        compare_world(orc, solver, sysm.ranks[0], P, g + 1)
+        Eo, Xo, reco = sysm.ranks[0].best()
+        Eg, Xg = solver.best()
+        assert Eg == Eo
+        np.testing.assert_array_equal(Xg, Xo)
+        st = solver.stats()
+        assert st.total_flips == sysm.ranks[0].total_flips
+        assert (st.best_algo, st.best_genop, st.best_generation, st.best_slot) == (
+            reco["algo"], reco["genop"], reco["gen"], reco["slot"])
+
+
+def test_k16_run_parity_and_optimum(orc, lib):
+    """Config K16: single search; GPU run == oracle run, and it reaches the
+    brute-force optimum over all 65536 vectors."""
+    import itertools
+    from paper_2207_03069_b200 import workloads as wl
+    U = wl.random_dense(16, 1)
+    X = np.array(list(itertools.product([0, 1], repeat=16)), np.int64)
+    opt = int(np.einsum("bi,ij,bj->b", X, U.astype(np.int64), X).min())
+    cfg = orc.Config(s_milli=100, b_milli=10000, pools=1, slots=1)
+    Eo, Xo, _ = orc.System(U, cfg).run(seed=1, flip_budget=10**9, target=opt)
+    solver = lib.Solver(U, s_milli=100, b_milli=10000, pools=1, slots=1, target=opt)
+    Eg, Xg = solver.run(seed=1, flip_budget=10**9)
+    assert Eg == Eo == opt
+    np.testing.assert_array_equal(Xg, Xo)
+
+
+SAMPLED = [("GS800", 2), ("TSP32", 2), ("K2000s", 2)]
+
+
+@pytest.mark.parametrize("config,gens", SAMPLED)
+def test_full_size_sampled_parity(orc, lib, config, gens):
+    """Bench launch configuration (auto slots, one pool): run generations on the
+    GPU, then recompute sampled slots' batches of the last generation on the
+    oracle from the pre-generation state."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make(config, seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1)
+    solver.reset(7)
+    for _ in range(gens - 1):
+        solver.generation()
+    rng = np.random.default_rng(0)
+    sample = sorted(set([0, solver.slots - 1] + list(rng.integers(0, solver.slots, 4))))
+    pre = {s: solver.read_slot(s) for s in sample}
+    solver.generation()
+    for s in sample:
+        pk = solver.read_packet(s)
+        post = solver.read_slot(s)
+        st = orc.SlotState(pre[s]["x"].copy(), pre[s]["delta"].copy(), pre[s]["E"], pre[s]["ring"].copy())
+        ref = orc.batch(U, st, pk["D"], pk["algo"], T=solver.T, B=solver.B, tabu=8, seed=7, slot=s,
+                        gen=gens - 1)
+        assert ref.flips == pk["flips"]
+        assert ref.ebest == pk["ebest"]
+        np.testing.assert_array_equal(ref.best, pk["best"])
+        np.testing.assert_array_equal(st.x, post["x"])
+        np.testing.assert_array_equal(st.delta, post["delta"])
+        assert st.E == post["E"]
+
+
+def test_r32k_sampled_parity(orc, lib):
+    """Config R32K at full size (2 GiB W): one sampled slot of the bench launch
+    recomputed by the oracle."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("R32K", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1)
+    solver.reset(3)
+    s = solver.slots // 2
+    pre = solver.read_slot(s)
+    solver.generation()
+    pk = solver.read_packet(s)
+    post = solver.read_slot(s)
+    st = orc.SlotState(pre["x"].copy(), pre["delta"].copy(), pre["E"], pre["ring"].copy())
+    ref = orc.batch(U, st, pk["D"], pk["algo"], T=solver.T, B=solver.B, tabu=8, seed=3, slot=s, gen=0)
+    assert ref.flips == pk["flips"] and ref.ebest == pk["ebest"]
+    np.testing.assert_array_equal(ref.best, pk["best"])
+    np.testing.assert_array_equal(st.x, post["x"])
+    np.testing.assert_array_equal(st.delta, post["delta"])
+    # property at any size: E(BEST) equals Eq.(2) evaluated directly on the device
+    assert solver.energy(pk["best"]) == pk["ebest"]
