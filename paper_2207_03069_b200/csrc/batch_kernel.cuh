@@ -3,13 +3,17 @@
 // A CTA of NT threads owns one search (one slot).  Element k of the search
 // lives in thread t = (k/8) mod NT, chunk c = (k/8) / NT, lane-of-chunk e = k mod 8,
 // so every thread holds EPT = 8*C flip gains Delta_k in REGISTERS and the bits
-// x_k, d_k of its elements in one bits_t word.  A flip of bit i streams row i
-// of the symmetric int16 W (2*n_pad bytes) with one coalesced 128-bit load per
-// thread and chunk, updates every Delta_k (Eq.(4)),
-// then Step 1 (scan, BEST) and Step 2 (selection) reduce
-// over the CTA with redux.sync + one shared-memory exchange.
+// x_k, d_k of its elements in one bits_t word.
 //
-// MW=false: one warp per search (n <= 2048), no shared-memory reductions.
+// Per flip (Step 3):  one elected thread streams row i of the
+// symmetric int16 W (2*n_pad bytes) from L2/HBM into shared
+// memory with cp.async.bulk (TMA engine, mbarrier completion, NP pieces so the
+// update of the first chunks overlaps the tail of the transfer); every thread
+// then applies Eq.(4) to its registers.  Step 1 (scan, BEST;
+// P:376-379) and Step 2 (selection) reduce over the CTA with
+// redux.sync + one shared-memory exchange (one __syncthreads per argmin).
+//
+// MW=false: one warp per search (n <= 2048), no CTA barriers at all.
 // MW=true : NT in {64..512} threads per search (n <= 32768).
 //
 // Citations: P:n = PAPER.md line n; R-x = DESIGN.md readings.
@@ -47,6 +51,44 @@ struct BatchParams {
     int64_t tr_cap;
 };
 
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one elected thread: expect `bytes` on mbarrier m and start the bulk copy
+__device__ __forceinline__ void bulk_row_piece(void* dst, const void* src, uint32_t bytes, uint64_t* m)
+{
+    asm volatile(
+        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(m))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+
 enum : int { OP_MIN = 0, OP_MAX = 1, OP_ADD = 2, OP_OR = 3 };
 
 __device__ __forceinline__ int wop(int op, int v)
@@ -65,8 +107,8 @@ __device__ __forceinline__ int op_ident(int op)
 
 constexpr int RED_W = 10;   // values per warp in one shared-memory exchange
 
-// Reduce K values over the CTA; every thread gets the results.  One
-// __syncthreads per call (MW); the buffer parity alternates with rc.
+// Reduce K values over the CTA; every thread gets the results.  Slots marked
+// OP_ARGKEY-style pairs are handled by the caller.  One __syncthreads (MW).
 template <bool MW, int K>
 __device__ __forceinline__ void block_reduce(int (&v)[K], const int (&ops)[K],
                                              int32_t (*red)[32][RED_W], int& rc, int lane, int wid,
@@ -90,28 +132,76 @@ __device__ __forceinline__ void block_reduce(int (&v)[K], const int (&ops)[K],
     }
 }
 
-// d[k] for a runtime k (one thread per warp at most executes these)
+// d[k] for a runtime k: jump table (one lane of a warp executes these)
 template <int EPT>
 __device__ __forceinline__ int get_at(const int32_t (&d)[EPT], int k)
 {
     int v = 0;
-#pragma unroll
-    for (int j = 0; j < EPT; j++)
-        if (j == k) v = d[j];
+    switch (k) {
+#define DABS_CASE(j) \
+    case j:          \
+        if constexpr (j < EPT) v = d[j]; \
+        break;
+        DABS_CASE(0) DABS_CASE(1) DABS_CASE(2) DABS_CASE(3) DABS_CASE(4) DABS_CASE(5) DABS_CASE(6) DABS_CASE(7)
+        DABS_CASE(8) DABS_CASE(9) DABS_CASE(10) DABS_CASE(11) DABS_CASE(12) DABS_CASE(13) DABS_CASE(14) DABS_CASE(15)
+        DABS_CASE(16) DABS_CASE(17) DABS_CASE(18) DABS_CASE(19) DABS_CASE(20) DABS_CASE(21) DABS_CASE(22) DABS_CASE(23)
+        DABS_CASE(24) DABS_CASE(25) DABS_CASE(26) DABS_CASE(27) DABS_CASE(28) DABS_CASE(29) DABS_CASE(30) DABS_CASE(31)
+        DABS_CASE(32) DABS_CASE(33) DABS_CASE(34) DABS_CASE(35) DABS_CASE(36) DABS_CASE(37) DABS_CASE(38) DABS_CASE(39)
+        DABS_CASE(40) DABS_CASE(41) DABS_CASE(42) DABS_CASE(43) DABS_CASE(44) DABS_CASE(45) DABS_CASE(46) DABS_CASE(47)
+        DABS_CASE(48) DABS_CASE(49) DABS_CASE(50) DABS_CASE(51) DABS_CASE(52) DABS_CASE(53) DABS_CASE(54) DABS_CASE(55)
+        DABS_CASE(56) DABS_CASE(57) DABS_CASE(58) DABS_CASE(59) DABS_CASE(60) DABS_CASE(61) DABS_CASE(62) DABS_CASE(63)
+#undef DABS_CASE
+    default: break;
+    }
     return v;
 }
 template <int EPT>
 __device__ __forceinline__ void neg_at(int32_t (&d)[EPT], int k)
 {
-#pragma unroll
-    for (int j = 0; j < EPT; j++)
-        if (j == k) d[j] = -d[j];
+    switch (k) {
+#define DABS_CASE(j) \
+    case j:          \
+        if constexpr (j < EPT) d[j] = -d[j]; \
+        break;
+        DABS_CASE(0) DABS_CASE(1) DABS_CASE(2) DABS_CASE(3) DABS_CASE(4) DABS_CASE(5) DABS_CASE(6) DABS_CASE(7)
+        DABS_CASE(8) DABS_CASE(9) DABS_CASE(10) DABS_CASE(11) DABS_CASE(12) DABS_CASE(13) DABS_CASE(14) DABS_CASE(15)
+        DABS_CASE(16) DABS_CASE(17) DABS_CASE(18) DABS_CASE(19) DABS_CASE(20) DABS_CASE(21) DABS_CASE(22) DABS_CASE(23)
+        DABS_CASE(24) DABS_CASE(25) DABS_CASE(26) DABS_CASE(27) DABS_CASE(28) DABS_CASE(29) DABS_CASE(30) DABS_CASE(31)
+        DABS_CASE(32) DABS_CASE(33) DABS_CASE(34) DABS_CASE(35) DABS_CASE(36) DABS_CASE(37) DABS_CASE(38) DABS_CASE(39)
+        DABS_CASE(40) DABS_CASE(41) DABS_CASE(42) DABS_CASE(43) DABS_CASE(44) DABS_CASE(45) DABS_CASE(46) DABS_CASE(47)
+        DABS_CASE(48) DABS_CASE(49) DABS_CASE(50) DABS_CASE(51) DABS_CASE(52) DABS_CASE(53) DABS_CASE(54) DABS_CASE(55)
+        DABS_CASE(56) DABS_CASE(57) DABS_CASE(58) DABS_CASE(59) DABS_CASE(60) DABS_CASE(61) DABS_CASE(62) DABS_CASE(63)
+#undef DABS_CASE
+    default: break;
+    }
+}
+// first lane-of-chunk e in chunk c with mask bit set and d == m (or -1)
+template <int EPT, typename bits_t>
+__device__ __forceinline__ int first_in_chunk(const int32_t (&d)[EPT], bits_t M, int c, int m)
+{
+    int r = -1;
+    switch (c) {
+#define DABS_CHUNK(cc)                                                                    \
+    case cc:                                                                              \
+        if constexpr (8 * cc < EPT) {                                                     \
+            _Pragma("unroll") for (int e = 7; e >= 0; e--) if (((M >> (8 * cc + e)) & 1) && \
+                                                                  d[8 * cc + e] == m) r = e; \
+        }                                                                                 \
+        break;
+        DABS_CHUNK(0) DABS_CHUNK(1) DABS_CHUNK(2) DABS_CHUNK(3)
+        DABS_CHUNK(4) DABS_CHUNK(5) DABS_CHUNK(6) DABS_CHUNK(7)
+#undef DABS_CHUNK
+    default: break;
+    }
+    return r;
 }
 
 template <int C, bool MW, bool TRACE>
 __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams p)
 {
     constexpr int EPT = 8 * C;
+    constexpr int NP = MW ? (C >= 4 ? 4 : C) : 1;   // row pieces, one mbarrier each
+    constexpr int CPP = C / NP;                      // chunks per piece
     using bits_t = typename std::conditional<(EPT > 32), unsigned long long, uint32_t>::type;
     constexpr bits_t ONE = 1;
     const int t = threadIdx.x;
@@ -122,6 +212,9 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     const uint32_t gslot = p.slot_base + (uint32_t)s;
     const int n = p.n;
 
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // one W row, 2*n_pad bytes
+    __shared__ __align__(8) uint64_t mbar[NP];
     __shared__ int32_t ring_s[TABU_RING];
     __shared__ int32_t red_s[2][32][RED_W];
     __shared__ int32_t bc_s[2][4];
@@ -147,19 +240,25 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
     }
     if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
+    if (t == 0) {
+#pragma unroll
+        for (int q = 0; q < NP; q++) mbar_init(&mbar[q], 1);
+        fence_mbar_init();
+    }
     int pos = 0;   // ring_s[(pos + j) & 31] = j-th most recent flip
     int64_t E = p.E[s];
     const int algo = p.algo[s];
+    const uint32_t piece_bytes = (uint32_t)(2 * p.n_pad / NP);
+    const char* Wbytes = reinterpret_cast<const char*>(p.W);
+    uint32_t par_row = 0;
     if constexpr (MW) __syncthreads(); else __syncwarp();
 
-    // element index of (chunk c, lane-of-chunk e) owned by this thread
     auto gidx = [&](int c, int e) { return (((c << lgNT) + t) << 3) | e; };
-    // bit position (in bits_t) of global element k, if this thread owns it
     auto owns = [&](int k) { return ((k >> 3) & (NT - 1)) == t; };
     auto lbit = [&](int k) { return (((k >> 3) >> lgNT) << 3) | (k & 7); };
 
-    // lowest (index<<1 | x) among this thread's elements in M with d == m
-    auto first_key = [&](bits_t M, int m) -> int {
+    // lowest (index<<1 | x) among this thread's elements in M with d == m (full scan; rare use)
+    auto first_key_full = [&](bits_t M, int m) -> int {
         int key = INT32_MAX;
 #pragma unroll
         for (int c = C - 1; c >= 0; c--) {
@@ -171,7 +270,16 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
         return key;
     };
-
+    // key of the first element with value m, given per-chunk minima gm[] (one lane runs it)
+    auto key_from_chunks = [&](const int (&gm)[C], bits_t M, int m) -> int {
+        int cs = 0;
+#pragma unroll
+        for (int c = C - 1; c >= 0; c--)
+            if (gm[c] == m) cs = c;
+        const int e = first_in_chunk(d, M, cs, m);
+        const int k = 8 * cs + e;
+        return (gidx(cs, e) << 1) | (int)((xb >> k) & 1);
+    };
     // tabu set = the last `tabu` flips (R-11)
     auto tabu_mask = [&]() -> bits_t {
         bits_t m = 0;
@@ -212,15 +320,53 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
     };
 
+    // CTA-wide (min, key) reduction of K1 argmin pairs plus K2 plain values,
+    // one exchange.  A pair is (tmin, key) where each thread contributes the
+    // key of its first element at the warp minimum (computed lazily by the
+    // lanes holding it).
+    auto reduce_pairs = [&](int (&vmin)[2], int (&vkey)[2], int np_, int (&ext)[4], const int (&eops)[4],
+                            int ne) {
+        // warp stage (vmin already warp-reduced, vkey already computed by the caller)
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+            if (k < np_) vkey[k] = warp_min(vkey[k]);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (k < ne) ext[k] = wop(eops[k], ext[k]);
+        if constexpr (MW) {
+            const int par = rc & 1;
+            rc++;
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < 2; k++)
+                    if (k < np_) { red_s[par][wid][2 * k] = vmin[k]; red_s[par][wid][2 * k + 1] = vkey[k]; }
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    if (k < ne) red_s[par][wid][4 + k] = ext[k];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                if (k < np_) {
+                    const int a = lane < NW ? red_s[par][lane][2 * k] : INT32_MAX;
+                    const int b = lane < NW ? red_s[par][lane][2 * k + 1] : INT32_MAX;
+                    vmin[k] = warp_min(a);
+                    vkey[k] = warp_min(a == vmin[k] ? b : INT32_MAX);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (k < ne) ext[k] = wop(eops[k], lane < NW ? red_s[par][lane][4 + k] : op_ident(eops[k]));
+        }
+    };
+
     // count + uniform pick in index order (MaxMin R-6, PositiveMin R-9):
-    // returns the pick via (si, sv, sx); kb = BEST key (lowest gmin index) if wanted.
-    auto locate_pick = [&](bits_t cb, uint32_t u, int kb_local, int& si, int& sv, int& sx,
-                           int& kb) {
-        int cnt[C], incl[C], woff[C], Tc[C];
+    // returns the pick via (si, sv, sx); kb = BEST key (lowest gmin index).
+    auto locate_pick = [&](bits_t cb, uint32_t u, int kb_local, int& si, int& sv, int& sx, int& kb) {
+        int incl[C];   // warp-inclusive prefix of this lane's candidate count, per chunk
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            cnt[c] = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-            int x = cnt[c];
+            int x = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, x, off);
@@ -228,8 +374,9 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             }
             incl[c] = x;
         }
+        int par = 0;
         if constexpr (MW) {
-            const int par = rc & 1;
+            par = rc & 1;
             rc++;
             const int kw = warp_min(kb_local);
             if (lane == 31) {
@@ -238,8 +385,17 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             }
             if (lane == 0) red_s[par][wid][RED_W - 1] = kw;
             __syncthreads();
+            kb = warp_min(lane < NW ? red_s[par][lane][RED_W - 1] : INT32_MAX);
+        } else {
+            kb = warp_min(kb_local);
+        }
+        // chunk-major order: all of chunk 0 (thread order), then chunk 1, ...
+        int tot = 0;
+        int li = -1;
 #pragma unroll
-            for (int c = 0; c < C; c++) {
+        for (int c = 0; c < C; c++) {
+            int woff = 0, Tc;
+            if constexpr (MW) {
                 const int x = lane < NW ? red_s[par][lane][c] : 0;
                 int y = x;
 #pragma unroll
@@ -247,46 +403,41 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                     const int z = __shfl_up_sync(0xffffffffu, y, off);
                     if (lane >= off) y += z;
                 }
-                woff[c] = __shfl_sync(0xffffffffu, y - x, wid);
-                Tc[c] = __shfl_sync(0xffffffffu, y, 31);
+                woff = __shfl_sync(0xffffffffu, y - x, wid);
+                Tc = __shfl_sync(0xffffffffu, y, 31);
+            } else {
+                Tc = __shfl_sync(0xffffffffu, incl[c], 31);
             }
-            kb = warp_min(lane < NW ? red_s[par][lane][RED_W - 1] : INT32_MAX);
-        } else {
-#pragma unroll
-            for (int c = 0; c < C; c++) {
-                woff[c] = 0;
-                Tc[c] = __shfl_sync(0xffffffffu, incl[c], 31);
-            }
-            kb = warp_min(kb_local);
+            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
+            const int lo = tot + woff + incl[c] - cnt;
+            incl[c] = lo;                          // reuse: start rank of this lane's chunk c
+            tot += Tc;
         }
-        uint32_t tot = 0;
-        int li = -1;
-        int Pc[C];
-#pragma unroll
-        for (int c = 0; c < C; c++) { Pc[c] = (int)tot; tot += (uint32_t)Tc[c]; }
-        const int r = (int)pick_u(u, tot);
+        const int r = (int)pick_u(u, (uint32_t)tot);
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const int lo = Pc[c] + woff[c] + incl[c] - cnt[c];
-            if (r >= lo && r < lo + cnt[c]) {
+            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
+            const int lo = incl[c];
+            if (r >= lo && r < lo + cnt) {
                 uint32_t byte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
                 for (int j = 0; j < r - lo; j++) byte &= byte - 1;   // drop lower set bits
-                const int e = __ffs(byte) - 1;
-                li = 8 * c + e;
+                li = 8 * c + (__ffs(byte) - 1);
             }
         }
         int gi = -1, lv = 0, lx = 0;
-        if (li >= 0) {
-            gi = gidx(li >> 3, li & 7);
-            lv = get_at(d, li);
-            lx = (int)((xb >> li) & 1);
+        if (__any_sync(0xffffffffu, li >= 0)) {
+            if (li >= 0) {
+                gi = gidx(li >> 3, li & 7);
+                lv = get_at(d, li);
+                lx = (int)((xb >> li) & 1);
+            }
         }
         if constexpr (MW) {
-            const int par = rc & 1;
+            const int par2 = rc & 1;
             rc++;
-            if (li >= 0) { bc_s[par][0] = gi; bc_s[par][1] = lv; bc_s[par][2] = lx; }
+            if (li >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
             __syncthreads();
-            si = bc_s[par][0]; sv = bc_s[par][1]; sx = bc_s[par][2];
+            si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
         } else {
             const int src = __ffs(__ballot_sync(0xffffffffu, li >= 0)) - 1;
             si = __shfl_sync(0xffffffffu, gi, src);
@@ -295,48 +446,152 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
     };
 
+    // lazy key of the global-min element for BEST (rare): lanes holding gmin
+    auto best_key = [&](int tg, int gmin) -> int {
+        int k = INT32_MAX;
+        if (__any_sync(0xffffffffu, tg == gmin)) {
+            if (tg == gmin) k = first_key_full(vb, gmin);
+        }
+        int v[1] = {k};
+        const int ops[1] = {OP_MIN};
+        block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+        return v[0];
+    };
+
     while (true) {
         int si = -1, sv = 0, sx = 0;       // selected bit, its Delta, its x (uniform)
         if (phase == 3) break;
 
         // ---------------- Step 1 + Step 2 per phase
-        if (phase == 1) {
-            // Greedy: argmin over all bits; stop when min >= 0 (R-4)
-            int tg = INT32_MAX;
+        if (phase == 1 || phase == 0 || (phase == 2 && (algo == ALG_CYCLIC || algo == ALG_RANDOM))) {
+            // argmin rules: Greedy, Straight, CyclicMin
+            // (R-7), RandomMin (R-8).  One exchange:
+            // (rule min, key), (global min, -), flags.
+            bits_t M1, M2 = 0;     // primary mask, fallback mask
+            int fb_mode = 0;       // 0 none, 1 fallback to M2, 2 fallback M2 then all
+            if (phase == 1) {
+                M1 = vb;
+            } else if (phase == 0) {
+                M1 = (xb ^ db) & vb;
+            } else {
+                if (tt == p.T) { end_phase(); continue; }
+                tt++;
+                const bits_t tm = tabu_mask();
+                if (algo == ALG_CYCLIC) {
+                    const int w = p.wtab[tt];
+                    const int b0 = min(cursor + w, n), b1 = cursor + w - n;
+                    bits_t wm = 0;
 #pragma unroll
-            for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
-            int v[1] = {tg};
-            const int ops[1] = {OP_MIN};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            const int gmin = v[0];
-            const bool best_upd = E + gmin < ebest;
-            if (gmin >= 0 && !best_upd) { end_phase(); continue; }
-            int kv[1] = {tg == gmin ? first_key(vb, gmin) : INT32_MAX};
-            block_reduce<MW>(kv, ops, red_s, rc, lane, wid, NW);
-            if (best_upd) set_best(kv[0], gmin);
-            if (gmin >= 0) { end_phase(); continue; }
-            si = kv[0] >> 1; sx = kv[0] & 1; sv = gmin;
-        } else if (phase == 0) {
-            // Straight: argmin over bits with x != d (R-5)
-            const bits_t cm = (xb ^ db) & vb;
-            int tg = INT32_MAX, ts = INT32_MAX;
+                    for (int c = 0; c < C; c++) {
+                        const int base = gidx(c, 0);
+                        const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
+                        if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
+                        const int hi2 = min(b1 - base, 8);
+                        if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
+                    }
+                    cursor = (cursor + w) % n;
+                    M1 = wm & ~tm;
+                    M2 = wm;
+                    fb_mode = 1;
+                } else {
+                    const uint32_t p16 = (uint32_t)p.ptab[tt];
+                    bits_t cand;
+                    if (p16 >= 65536u) {
+                        cand = vb;
+                    } else {
+                        cand = 0;
 #pragma unroll
-            for (int k = 0; k < EPT; k++) {
-                tg = min(tg, d[k]);
-                if ((cm >> k) & 1) ts = min(ts, d[k]);
+                        for (int c = 0; c < C; c++) {
+                            const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot,
+                                                 p.gen, (uint32_t)flips);
+                            const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
+                            uint32_t byte = 0;
+#pragma unroll
+                            for (int e = 0; e < 8; e++) {
+                                const uint32_t u16 = (wds[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                                byte |= (uint32_t)(u16 < p16) << e;
+                            }
+                            cand |= (bits_t)byte << (8 * c);
+                        }
+                    }
+                    M1 = cand & ~tm & vb;
+                    M2 = ~tm & vb;
+                    fb_mode = 2;
+                }
             }
-            int v[3] = {tg, ts, cm != 0};
-            const int ops[3] = {OP_MIN, OP_MIN, OP_OR};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            if (!v[2]) { end_phase(); continue; }
-            const int gmin = v[0];
+            // scan: the global minimum (Step 1) and per-chunk minima of the
+            // rule's candidate set M1 (Greedy: all bits).  Warps whose lanes
+            // hold no candidate skip the masked scan (CyclicMin reads only its
+            // window).  The fallback set M2 is scanned lazily.
+            const bool use_g = (phase == 1);
+            int gsel[C];
+            int tg = INT32_MAX, t1 = INT32_MAX;
+            if (use_g) {
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    int mg = INT32_MAX;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) mg = min(mg, d[8 * c + e]);
+                    gsel[c] = mg;
+                    tg = min(tg, mg);
+                }
+                t1 = tg;
+            } else {
+#pragma unroll
+                for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
+#pragma unroll
+                for (int c = 0; c < C; c++) gsel[c] = INT32_MAX;
+                if (__any_sync(0xffffffffu, M1 != 0)) {
+#pragma unroll
+                    for (int c = 0; c < C; c++) {
+                        int m1 = INT32_MAX;
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            if ((M1 >> (8 * c + e)) & 1) m1 = min(m1, d[8 * c + e]);
+                        gsel[c] = m1;
+                        t1 = min(t1, m1);
+                    }
+                }
+            }
+            // warp minimum and lazy key (only the lanes holding it search)
+            int vmin[2], vkey[2] = {INT32_MAX, INT32_MAX};
+            vmin[0] = warp_min(t1);
+            if (__any_sync(0xffffffffu, t1 == vmin[0] && vmin[0] != INT32_MAX))
+                if (t1 == vmin[0] && vmin[0] != INT32_MAX)
+                    vkey[0] = key_from_chunks(gsel, use_g ? ~(bits_t)0 : M1, vmin[0]);
+            int ext[4] = {tg, 0, 0, 0};
+            const int eops[4] = {OP_MIN, OP_MIN, OP_MIN, OP_MIN};
+            reduce_pairs(vmin, vkey, 1, ext, eops, 1);
+            const int gmin = ext[0];
+            int m = vmin[0], key = vkey[0];
+            if (m == INT32_MAX && fb_mode) {
+                // empty candidate set: CyclicMin window all tabu (R-7) / RandomMin
+                // with no candidate (R-8) -> argmin over M2 (then over all bits)
+                int t2 = INT32_MAX;
+#pragma unroll
+                for (int k = 0; k < EPT; k++)
+                    if ((M2 >> k) & 1) t2 = min(t2, d[k]);
+                int v2[1] = {t2};
+                const int ops1[1] = {OP_MIN};
+                block_reduce<MW>(v2, ops1, red_s, rc, lane, wid, NW);
+                if (v2[0] != INT32_MAX) {
+                    m = v2[0];
+                    int k2 = INT32_MAX;
+                    if (__any_sync(0xffffffffu, t2 == m))
+                        if (t2 == m) k2 = first_key_full(M2, m);
+                    int kv[1] = {k2};
+                    block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
+                    key = kv[0];
+                } else {
+                    m = gmin;
+                    key = best_key(tg, gmin);
+                }
+            }
+            if (phase == 0 && m == INT32_MAX) { end_phase(); continue; }   // X == D
             const bool best_upd = E + gmin < ebest;
-            int kv[2] = {ts == v[1] ? first_key(cm, v[1]) : INT32_MAX,
-                         (best_upd && tg == gmin) ? first_key(vb, gmin) : INT32_MAX};
-            const int ops2[2] = {OP_MIN, OP_MIN};
-            block_reduce<MW>(kv, ops2, red_s, rc, lane, wid, NW);
-            if (best_upd) set_best(kv[1], gmin);
-            si = kv[0] >> 1; sx = kv[0] & 1; sv = v[1];
+            if (best_upd) set_best(use_g ? key : best_key(tg, gmin), gmin);
+            if (phase == 1 && gmin >= 0) { end_phase(); continue; }       // R-4
+            si = key >> 1; sx = key & 1; sv = m;
         } else if (algo == ALG_TWO) {
             // TwoNeighbor (R-10): 0, then (k, k-1) for k = 1..n-1
             if (q == 2 * n - 1) { end_phase(); continue; }
@@ -347,9 +602,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
             int ov = 0, ox = 0;
             const bool own = owns(i);
-            if (own) {
-                ov = get_at(d, lbit(i));
-                ox = (int)((xb >> lbit(i)) & 1);
+            if (__any_sync(0xffffffffu, own)) {
+                if (own) {
+                    ov = get_at(d, lbit(i));
+                    ox = (int)((xb >> lbit(i)) & 1);
+                }
             }
             if constexpr (MW) {
                 if (own) { bc_s[rc & 1][0] = ov; bc_s[rc & 1][1] = ox; }
@@ -366,11 +623,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 ox = __shfl_sync(0xffffffffu, ox, src);
             }
             const int gmin = v[0];
-            if (E + gmin < ebest) {
-                int kv[1] = {tg == gmin ? first_key(vb, gmin) : INT32_MAX};
-                block_reduce<MW>(kv, ops, red_s, rc, lane, wid, NW);
-                set_best(kv[0], gmin);
-            }
+            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
             si = i; sv = ov; sx = ox;
         } else {
             if (tt == p.T) { end_phase(); continue; }
@@ -378,88 +631,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             const bits_t tm = tabu_mask();
             const bits_t el = ~tm & vb;
             int tg = INT32_MAX;
-            if (algo == ALG_CYCLIC) {
-                // CyclicMin (R-7): window [cursor, cursor + w) mod n
-                const int w = p.wtab[tt];
-                const int b0 = min(cursor + w, n), b1 = cursor + w - n;
-                bits_t wm = 0;
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    const int base = gidx(c, 0);
-                    const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
-                    if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
-                    const int hi2 = min(b1 - base, 8);
-                    if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
-                }
-                cursor = (cursor + w) % n;
-                const bits_t m1 = wm & ~tm;
-                int t1 = INT32_MAX, t2 = INT32_MAX;
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if ((m1 >> k) & 1) t1 = min(t1, d[k]);
-                    if ((wm >> k) & 1) t2 = min(t2, d[k]);
-                }
-                int v[4] = {tg, t1, m1 != 0, t2};
-                const int ops[4] = {OP_MIN, OP_MIN, OP_OR, OP_MIN};
-                block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-                const int gmin = v[0];
-                const bool best_upd = E + gmin < ebest;
-                const bool use1 = v[2] != 0;
-                const int m = use1 ? v[1] : v[3];
-                const int tmine = use1 ? t1 : t2;
-                int kv[2] = {tmine == m ? first_key(use1 ? m1 : wm, m) : INT32_MAX,
-                             (best_upd && tg == gmin) ? first_key(vb, gmin) : INT32_MAX};
-                const int ops2[2] = {OP_MIN, OP_MIN};
-                block_reduce<MW>(kv, ops2, red_s, rc, lane, wid, NW);
-                if (best_upd) set_best(kv[1], gmin);
-                si = kv[0] >> 1; sx = kv[0] & 1; sv = m;
-            } else if (algo == ALG_RANDOM) {
-                // RandomMin (R-8): Philox candidates, argmin
-                const uint32_t p16 = (uint32_t)p.ptab[tt];
-                bits_t cand;
-                if (p16 >= 65536u) {
-                    cand = vb;
-                } else {
-                    cand = 0;
-#pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot,
-                                             p.gen, (uint32_t)flips);
-                        const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
-                        uint32_t byte = 0;
-#pragma unroll
-                        for (int e = 0; e < 8; e++) {
-                            const uint32_t u16 = (wds[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                            byte |= (uint32_t)(u16 < p16) << e;
-                        }
-                        cand |= (bits_t)byte << (8 * c);
-                    }
-                }
-                const bits_t m1 = cand & el;
-                int t1 = INT32_MAX, t2 = INT32_MAX;
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if ((m1 >> k) & 1) t1 = min(t1, d[k]);
-                    if ((el >> k) & 1) t2 = min(t2, d[k]);
-                }
-                int v[5] = {tg, t1, m1 != 0, t2, el != 0};
-                const int ops[5] = {OP_MIN, OP_MIN, OP_OR, OP_MIN, OP_OR};
-                block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-                const int gmin = v[0];
-                const bool best_upd = E + gmin < ebest;
-                const int which = v[2] ? 0 : (v[4] ? 1 : 2);
-                const int m = which == 0 ? v[1] : (which == 1 ? v[3] : gmin);
-                const bits_t M = which == 0 ? m1 : (which == 1 ? el : vb);
-                const int tmine = which == 0 ? t1 : (which == 1 ? t2 : tg);
-                int kv[2] = {tmine == m ? first_key(M, m) : INT32_MAX,
-                             (best_upd && tg == gmin) ? first_key(vb, gmin) : INT32_MAX};
-                const int ops2[2] = {OP_MIN, OP_MIN};
-                block_reduce<MW>(kv, ops2, red_s, rc, lane, wid, NW);
-                if (best_upd) set_best(kv[1], gmin);
-                si = kv[0] >> 1; sx = kv[0] & 1; sv = m;
-            } else if (algo == ALG_MAXMIN) {
+            if (algo == ALG_MAXMIN) {
                 // MaxMin (R-6)
                 int lo = INT32_MAX, hi = INT32_MIN, hv = INT32_MIN;
 #pragma unroll
@@ -485,9 +657,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 for (int k = 0; k < EPT; k++)
                     if ((int64_t)d[k] <= thr) cb |= ONE << k;
                 cb &= EL;
+                int kbl = INT32_MAX;
+                if (best_upd && __any_sync(0xffffffffu, tg == gmin))
+                    if (tg == gmin) kbl = first_key_full(vb, gmin);
                 int kb;
-                locate_pick(cb, r.y, (best_upd && tg == gmin) ? first_key(vb, gmin) : INT32_MAX,
-                            si, sv, sx, kb);
+                locate_pick(cb, r.y, kbl, si, sv, sx, kb);
                 if (best_upd) set_best(kb, gmin);
             } else {
                 // PositiveMin (R-9)
@@ -513,26 +687,34 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                     if (d[k] <= pm) cb |= ONE << k;
                 cb &= EL;
                 const uint4 r = rng4(p.seed, PUR_POSMIN, 0, gslot, p.gen, (uint32_t)flips);
+                int kbl = INT32_MAX;
+                if (best_upd && __any_sync(0xffffffffu, tg == gmin))
+                    if (tg == gmin) kbl = first_key_full(vb, gmin);
                 int kb;
-                locate_pick(cb, r.x, (best_upd && tg == gmin) ? first_key(vb, gmin) : INT32_MAX,
-                            si, sv, sx, kb);
+                locate_pick(cb, r.x, kbl, si, sv, sx, kb);
                 if (best_upd) set_best(kb, gmin);
             }
         }
 
         // ---------------- Step 3: flip bit si
-        const uint4* row = reinterpret_cast<const uint4*>(p.W + (size_t)si * p.n_pad);
-        uint4 rw[C];
+        // (every thread has passed the last exchange, so the row buffer is free)
+        if (t == 0) {
+            fence_proxy_async();
+            const char* src = Wbytes + (size_t)si * (size_t)(2 * p.n_pad);
 #pragma unroll
-        for (int c = 0; c < C; c++) rw[c] = __ldg(row + (c << lgNT) + t);
+            for (int qq = 0; qq < NP; qq++)
+                bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
+        }
         E += sv;
         // s_k = sigma(x_i) sigma(x_k) = -1 on these elements (Eq.(4))
         const bits_t negm = sx ? ~xb : xb;
-        if (owns(si)) {
-            const int k = lbit(si);
-            neg_at(d, k);                  // Eq.(5)
-            xb ^= ONE << k;
-            bdiff ^= ONE << k;
+        if (__any_sync(0xffffffffu, owns(si))) {
+            if (owns(si)) {
+                const int k = lbit(si);
+                neg_at(d, k);                  // Eq.(5)
+                xb ^= ONE << k;
+                bdiff ^= ONE << k;
+            }
         }
         pos = (pos + TABU_RING - 1) & (TABU_RING - 1);
         ring_s[pos] = si;
@@ -545,17 +727,26 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
         flips++;
 #pragma unroll
-        for (int c = 0; c < C; c++) {
-            const uint32_t wv[4] = {rw[c].x, rw[c].y, rw[c].z, rw[c].w};
+        for (int qq = 0; qq < NP; qq++) {
+            mbar_wait(&mbar[qq], par_row);
+            uint4 rw[CPP];
 #pragma unroll
-            for (int h = 0; h < 4; h++) {
-                const int lo = (int)(int16_t)(wv[h] & 0xFFFFu);
-                const int hi = (int)wv[h] >> 16;
-                const int k0 = 8 * c + 2 * h, k1 = k0 + 1;
-                d[k0] += ((negm >> k0) & 1) ? -lo : lo;
-                d[k1] += ((negm >> k1) & 1) ? -hi : hi;
+            for (int cc = 0; cc < CPP; cc++) rw[cc] = row_s[((qq * CPP + cc) << lgNT) + t];
+#pragma unroll
+            for (int cc = 0; cc < CPP; cc++) {
+                const int c = qq * CPP + cc;
+                const uint32_t wv[4] = {rw[cc].x, rw[cc].y, rw[cc].z, rw[cc].w};
+#pragma unroll
+                for (int h = 0; h < 4; h++) {
+                    const int lo = (int)(int16_t)(wv[h] & 0xFFFFu);
+                    const int hi = (int)wv[h] >> 16;
+                    const int k0 = 8 * c + 2 * h, k1 = k0 + 1;
+                    d[k0] += ((negm >> k0) & 1) ? -lo : lo;
+                    d[k1] += ((negm >> k1) & 1) ? -hi : hi;
+                }
             }
         }
+        par_row ^= 1u;
     }
 
     // ---------------- write back state and the result packet

@@ -160,6 +160,8 @@ static BatchFn pick_batch(int C, bool mw, bool trace)
     }
 }
 
+static size_t row_smem(const dabs_ctx* c) { return (size_t)2 * c->n_pad; }   // one W row
+
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
 {
     BatchParams p{};
@@ -253,6 +255,11 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
     }
     c->n_pad = c->NT * c->C * 8;
     c->nwp = c->n_pad / 32;
+    for (int tr = 0; tr < 2; tr++) {
+        cudaError_t e = cudaFuncSetAttribute(pick_batch(c->C, c->mw, tr != 0),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
+        if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
+    }
     c->T = flip_factor(cfg.s_milli, n);
     c->B = flip_factor(cfg.b_milli, n);
     c->tabu = (int)cfg.tabu_period;
@@ -262,7 +269,7 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
         c->S = (int)cfg.slots_per_pool;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->mw, false), c->NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->mw, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = prop.multiProcessorCount * occ;
         c->S = (2 * conc + c->P - 1) / c->P;   // about two waves per generation
@@ -428,7 +435,7 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
 {
     BatchParams p = batch_params(c, seed, gen, slot0);
     BatchFn fn = pick_batch(c->C, c->mw, trace);
-    fn<<<count, c->NT, 0, c->stream>>>(p);
+    fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
     CK(cudaGetLastError());
     return DABS_OK;
 }
