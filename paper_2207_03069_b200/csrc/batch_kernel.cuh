@@ -204,9 +204,10 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     constexpr int CPP = C / NP;                      // chunks per piece
     using bits_t = typename std::conditional<(EPT > 32), unsigned long long, uint32_t>::type;
     constexpr bits_t ONE = 1;
+    constexpr unsigned FULL = 0xffffffffu;
     const int t = threadIdx.x;
     const int NT = MW ? (int)blockDim.x : 32;
-    const int lgNT = 31 - __clz(NT);
+    const int lgNT = MW ? 31 - __clz(NT) : 5;
     const int lane = t & 31, wid = t >> 5, NW = NT >> 5;
     const int s = p.slot0 + (int)blockIdx.x;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
@@ -242,21 +243,58 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
     if (t == 0) {
 #pragma unroll
-        for (int q = 0; q < NP; q++) mbar_init(&mbar[q], 1);
+        for (int qq = 0; qq < NP; qq++) mbar_init(&mbar[qq], 1);
         fence_mbar_init();
     }
     int pos = 0;   // ring_s[(pos + j) & 31] = j-th most recent flip
     int64_t E = p.E[s];
     const int algo = p.algo[s];
+    const int tabu = p.tabu;
     const uint32_t piece_bytes = (uint32_t)(2 * p.n_pad / NP);
-    const char* Wbytes = reinterpret_cast<const char*>(p.W);
     uint32_t par_row = 0;
+    int flips = 0;
+    int64_t ebest = E_INF;
+    bits_t bdiff = 0;              // BEST = X xor bdiff
+    int rc = 0;                    // exchange parity counter
+    int phase_code = 0;            // for the trace: 0 Straight, 1 Greedy, 2+r main round r
     if constexpr (MW) __syncthreads(); else __syncwarp();
 
     auto gidx = [&](int c, int e) { return (((c << lgNT) + t) << 3) | e; };
     auto owns = [&](int k) { return ((k >> 3) & (NT - 1)) == t; };
     auto lbit = [&](int k) { return (((k >> 3) >> lgNT) << 3) | (k & 7); };
 
+    // ---------------- scans (Step 1 and the argmin rules of Step 2)
+    auto scan_min = [&]() -> int {            // min over all elements (pads are INT32_MAX)
+        int m = INT32_MAX;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) m = min(m, d[k]);
+        return m;
+    };
+    auto scan_chunks = [&](int (&gm)[C]) -> int {   // per-chunk minima, all elements
+        int m = INT32_MAX;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            int mc = INT32_MAX;
+#pragma unroll
+            for (int e = 0; e < 8; e++) mc = min(mc, d[8 * c + e]);
+            gm[c] = mc;
+            m = min(m, mc);
+        }
+        return m;
+    };
+    auto scan_chunks_masked = [&](bits_t M, int (&gm)[C]) -> int {   // per-chunk minima over M
+        int m = INT32_MAX;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            int mc = INT32_MAX;
+#pragma unroll
+            for (int e = 0; e < 8; e++)
+                if ((M >> (8 * c + e)) & 1) mc = min(mc, d[8 * c + e]);
+            gm[c] = mc;
+            m = min(m, mc);
+        }
+        return m;
+    };
     // lowest (index<<1 | x) among this thread's elements in M with d == m (full scan; rare use)
     auto first_key_full = [&](bits_t M, int m) -> int {
         int key = INT32_MAX;
@@ -270,7 +308,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
         return key;
     };
-    // key of the first element with value m, given per-chunk minima gm[] (one lane runs it)
+    // key of the first element with value m, from per-chunk minima (one lane runs it)
     auto key_from_chunks = [&](const int (&gm)[C], bits_t M, int m) -> int {
         int cs = 0;
 #pragma unroll
@@ -280,438 +318,81 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         const int k = 8 * cs + e;
         return (gidx(cs, e) << 1) | (int)((xb >> k) & 1);
     };
-    // tabu set = the last `tabu` flips (R-11)
-    auto tabu_mask = [&]() -> bits_t {
-        bits_t m = 0;
-        for (int j = 0; j < p.tabu; j++) {
-            const int r = ring_s[(pos + j) & (TABU_RING - 1)];
-            if (r >= 0 && owns(r)) m |= ONE << lbit(r);
-        }
-        return m;
-    };
-
-    int phase = 0;                 // 0 Straight, 1 Greedy, 2 main, 3 done
-    bool after_main = false;
-    int round = 0, tt = 0, cursor = 0, q = 0;
-    int flips = 0;
-    int64_t ebest = E_INF;
-    bits_t bdiff = 0;              // BEST = X xor bdiff
-    int rc = 0;
-
-    auto set_best = [&](int key, int m) {
-        ebest = E + m;
-        const int j = key >> 1;
-        bdiff = owns(j) ? (ONE << lbit(j)) : (bits_t)0;
-    };
-    auto end_phase = [&]() {
-        if (phase == 0) {
-            phase = 1;
-            after_main = false;
-        } else if (phase == 1) {
-            if (after_main && (algo == ALG_TWO || flips >= p.B)) {   // R-12
-                phase = 3;
-            } else {
-                if (after_main) round++;
-                phase = 2; tt = 0; cursor = 0; q = 0;
-            }
-        } else {
-            phase = 1;
-            after_main = true;
-        }
-    };
-
-    // CTA-wide (min, key) reduction of K1 argmin pairs plus K2 plain values,
-    // one exchange.  A pair is (tmin, key) where each thread contributes the
-    // key of its first element at the warp minimum (computed lazily by the
-    // lanes holding it).
-    auto reduce_pairs = [&](int (&vmin)[2], int (&vkey)[2], int np_, int (&ext)[4], const int (&eops)[4],
-                            int ne) {
-        // warp stage (vmin already warp-reduced, vkey already computed by the caller)
-#pragma unroll
-        for (int k = 0; k < 2; k++)
-            if (k < np_) vkey[k] = warp_min(vkey[k]);
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-            if (k < ne) ext[k] = wop(eops[k], ext[k]);
+    // One exchange: argmin (value, lowest key) of the rule + min of tg (Step 1).
+    auto argmin_exchange = [&](int tsel, const int (&gm)[C], bits_t M, int tg, int& m, int& key,
+                               int& gmin) {
+        const int wmin = warp_min(tsel);
+        int k = INT32_MAX;
+        if (__any_sync(FULL, tsel == wmin && wmin != INT32_MAX))
+            if (tsel == wmin && wmin != INT32_MAX) k = key_from_chunks(gm, M, wmin);
+        k = warp_min(k);
+        int g = warp_min(tg);
         if constexpr (MW) {
             const int par = rc & 1;
             rc++;
-            if (lane == 0) {
-#pragma unroll
-                for (int k = 0; k < 2; k++)
-                    if (k < np_) { red_s[par][wid][2 * k] = vmin[k]; red_s[par][wid][2 * k + 1] = vkey[k]; }
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (k < ne) red_s[par][wid][4 + k] = ext[k];
-            }
+            if (lane == 0) { red_s[par][wid][0] = wmin; red_s[par][wid][1] = k; red_s[par][wid][2] = g; }
             __syncthreads();
-#pragma unroll
-            for (int k = 0; k < 2; k++) {
-                if (k < np_) {
-                    const int a = lane < NW ? red_s[par][lane][2 * k] : INT32_MAX;
-                    const int b = lane < NW ? red_s[par][lane][2 * k + 1] : INT32_MAX;
-                    vmin[k] = warp_min(a);
-                    vkey[k] = warp_min(a == vmin[k] ? b : INT32_MAX);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; k++)
-                if (k < ne) ext[k] = wop(eops[k], lane < NW ? red_s[par][lane][4 + k] : op_ident(eops[k]));
+            const int a = lane < NW ? red_s[par][lane][0] : INT32_MAX;
+            const int b = lane < NW ? red_s[par][lane][1] : INT32_MAX;
+            const int c = lane < NW ? red_s[par][lane][2] : INT32_MAX;
+            m = warp_min(a);
+            key = warp_min(a == m ? b : INT32_MAX);
+            gmin = warp_min(c);
+        } else {
+            m = wmin;
+            key = k;
+            gmin = g;
         }
     };
-
-    // count + uniform pick in index order (MaxMin R-6, PositiveMin R-9):
-    // returns the pick via (si, sv, sx); kb = BEST key (lowest gmin index).
-    auto locate_pick = [&](bits_t cb, uint32_t u, int kb_local, int& si, int& sv, int& sx, int& kb) {
-        int incl[C];   // warp-inclusive prefix of this lane's candidate count, per chunk
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            int x = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, off);
-                if (lane >= off) x += y;
-            }
-            incl[c] = x;
-        }
-        int par = 0;
-        if constexpr (MW) {
-            par = rc & 1;
-            rc++;
-            const int kw = warp_min(kb_local);
-            if (lane == 31) {
-#pragma unroll
-                for (int c = 0; c < C; c++) red_s[par][wid][c] = incl[c];
-            }
-            if (lane == 0) red_s[par][wid][RED_W - 1] = kw;
-            __syncthreads();
-            kb = warp_min(lane < NW ? red_s[par][lane][RED_W - 1] : INT32_MAX);
-        } else {
-            kb = warp_min(kb_local);
-        }
-        // chunk-major order: all of chunk 0 (thread order), then chunk 1, ...
-        int tot = 0;
-        int li = -1;
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            int woff = 0, Tc;
-            if constexpr (MW) {
-                const int x = lane < NW ? red_s[par][lane][c] : 0;
-                int y = x;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int z = __shfl_up_sync(0xffffffffu, y, off);
-                    if (lane >= off) y += z;
-                }
-                woff = __shfl_sync(0xffffffffu, y - x, wid);
-                Tc = __shfl_sync(0xffffffffu, y, 31);
-            } else {
-                Tc = __shfl_sync(0xffffffffu, incl[c], 31);
-            }
-            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-            const int lo = tot + woff + incl[c] - cnt;
-            incl[c] = lo;                          // reuse: start rank of this lane's chunk c
-            tot += Tc;
-        }
-        const int r = (int)pick_u(u, (uint32_t)tot);
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-            const int lo = incl[c];
-            if (r >= lo && r < lo + cnt) {
-                uint32_t byte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
-                for (int j = 0; j < r - lo; j++) byte &= byte - 1;   // drop lower set bits
-                li = 8 * c + (__ffs(byte) - 1);
-            }
-        }
-        int gi = -1, lv = 0, lx = 0;
-        if (__any_sync(0xffffffffu, li >= 0)) {
-            if (li >= 0) {
-                gi = gidx(li >> 3, li & 7);
-                lv = get_at(d, li);
-                lx = (int)((xb >> li) & 1);
-            }
-        }
-        if constexpr (MW) {
-            const int par2 = rc & 1;
-            rc++;
-            if (li >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
-            __syncthreads();
-            si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
-        } else {
-            const int src = __ffs(__ballot_sync(0xffffffffu, li >= 0)) - 1;
-            si = __shfl_sync(0xffffffffu, gi, src);
-            sv = __shfl_sync(0xffffffffu, lv, src);
-            sx = __shfl_sync(0xffffffffu, lx, src);
-        }
-    };
-
-    // lazy key of the global-min element for BEST (rare): lanes holding gmin
+    // lazy key of the global-min element (BEST update, rare)
     auto best_key = [&](int tg, int gmin) -> int {
         int k = INT32_MAX;
-        if (__any_sync(0xffffffffu, tg == gmin)) {
+        if (__any_sync(FULL, tg == gmin))
             if (tg == gmin) k = first_key_full(vb, gmin);
-        }
         int v[1] = {k};
         const int ops[1] = {OP_MIN};
         block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
         return v[0];
     };
+    // masked argmin over M with a full-scan key (fallback paths, rare)
+    auto argmin_slow = [&](bits_t M, int& m, int& key) {
+        int tm_ = INT32_MAX;
+#pragma unroll
+        for (int k = 0; k < EPT; k++)
+            if ((M >> k) & 1) tm_ = min(tm_, d[k]);
+        int v[1] = {tm_};
+        const int ops[1] = {OP_MIN};
+        block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+        m = v[0];
+        int kk = INT32_MAX;
+        if (__any_sync(FULL, tm_ == m && m != INT32_MAX))
+            if (tm_ == m && m != INT32_MAX) kk = first_key_full(M, m);
+        int kv[1] = {kk};
+        block_reduce<MW>(kv, ops, red_s, rc, lane, wid, NW);
+        key = kv[0];
+    };
+    auto set_best = [&](int key, int m) {
+        ebest = E + m;
+        const int j = key >> 1;
+        bdiff = owns(j) ? (ONE << lbit(j)) : (bits_t)0;
+    };
 
-    while (true) {
-        int si = -1, sv = 0, sx = 0;       // selected bit, its Delta, its x (uniform)
-        if (phase == 3) break;
-
-        // ---------------- Step 1 + Step 2 per phase
-        if (phase == 1 || phase == 0 || (phase == 2 && (algo == ALG_CYCLIC || algo == ALG_RANDOM))) {
-            // argmin rules: Greedy, Straight, CyclicMin
-            // (R-7), RandomMin (R-8).  One exchange:
-            // (rule min, key), (global min, -), flags.
-            bits_t M1, M2 = 0;     // primary mask, fallback mask
-            int fb_mode = 0;       // 0 none, 1 fallback to M2, 2 fallback M2 then all
-            if (phase == 1) {
-                M1 = vb;
-            } else if (phase == 0) {
-                M1 = (xb ^ db) & vb;
-            } else {
-                if (tt == p.T) { end_phase(); continue; }
-                tt++;
-                const bits_t tm = tabu_mask();
-                if (algo == ALG_CYCLIC) {
-                    const int w = p.wtab[tt];
-                    const int b0 = min(cursor + w, n), b1 = cursor + w - n;
-                    bits_t wm = 0;
-#pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        const int base = gidx(c, 0);
-                        const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
-                        if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
-                        const int hi2 = min(b1 - base, 8);
-                        if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
-                    }
-                    cursor = (cursor + w) % n;
-                    M1 = wm & ~tm;
-                    M2 = wm;
-                    fb_mode = 1;
-                } else {
-                    const uint32_t p16 = (uint32_t)p.ptab[tt];
-                    bits_t cand;
-                    if (p16 >= 65536u) {
-                        cand = vb;
-                    } else {
-                        cand = 0;
-#pragma unroll
-                        for (int c = 0; c < C; c++) {
-                            const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot,
-                                                 p.gen, (uint32_t)flips);
-                            const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
-                            uint32_t byte = 0;
-#pragma unroll
-                            for (int e = 0; e < 8; e++) {
-                                const uint32_t u16 = (wds[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                                byte |= (uint32_t)(u16 < p16) << e;
-                            }
-                            cand |= (bits_t)byte << (8 * c);
-                        }
-                    }
-                    M1 = cand & ~tm & vb;
-                    M2 = ~tm & vb;
-                    fb_mode = 2;
-                }
-            }
-            // scan: the global minimum (Step 1) and per-chunk minima of the
-            // rule's candidate set M1 (Greedy: all bits).  Warps whose lanes
-            // hold no candidate skip the masked scan (CyclicMin reads only its
-            // window).  The fallback set M2 is scanned lazily.
-            const bool use_g = (phase == 1);
-            int gsel[C];
-            int tg = INT32_MAX, t1 = INT32_MAX;
-            if (use_g) {
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    int mg = INT32_MAX;
-#pragma unroll
-                    for (int e = 0; e < 8; e++) mg = min(mg, d[8 * c + e]);
-                    gsel[c] = mg;
-                    tg = min(tg, mg);
-                }
-                t1 = tg;
-            } else {
-#pragma unroll
-                for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
-#pragma unroll
-                for (int c = 0; c < C; c++) gsel[c] = INT32_MAX;
-                if (__any_sync(0xffffffffu, M1 != 0)) {
-#pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        int m1 = INT32_MAX;
-#pragma unroll
-                        for (int e = 0; e < 8; e++)
-                            if ((M1 >> (8 * c + e)) & 1) m1 = min(m1, d[8 * c + e]);
-                        gsel[c] = m1;
-                        t1 = min(t1, m1);
-                    }
-                }
-            }
-            // warp minimum and lazy key (only the lanes holding it search)
-            int vmin[2], vkey[2] = {INT32_MAX, INT32_MAX};
-            vmin[0] = warp_min(t1);
-            if (__any_sync(0xffffffffu, t1 == vmin[0] && vmin[0] != INT32_MAX))
-                if (t1 == vmin[0] && vmin[0] != INT32_MAX)
-                    vkey[0] = key_from_chunks(gsel, use_g ? ~(bits_t)0 : M1, vmin[0]);
-            int ext[4] = {tg, 0, 0, 0};
-            const int eops[4] = {OP_MIN, OP_MIN, OP_MIN, OP_MIN};
-            reduce_pairs(vmin, vkey, 1, ext, eops, 1);
-            const int gmin = ext[0];
-            int m = vmin[0], key = vkey[0];
-            if (m == INT32_MAX && fb_mode) {
-                // empty candidate set: CyclicMin window all tabu (R-7) / RandomMin
-                // with no candidate (R-8) -> argmin over M2 (then over all bits)
-                int t2 = INT32_MAX;
-#pragma unroll
-                for (int k = 0; k < EPT; k++)
-                    if ((M2 >> k) & 1) t2 = min(t2, d[k]);
-                int v2[1] = {t2};
-                const int ops1[1] = {OP_MIN};
-                block_reduce<MW>(v2, ops1, red_s, rc, lane, wid, NW);
-                if (v2[0] != INT32_MAX) {
-                    m = v2[0];
-                    int k2 = INT32_MAX;
-                    if (__any_sync(0xffffffffu, t2 == m))
-                        if (t2 == m) k2 = first_key_full(M2, m);
-                    int kv[1] = {k2};
-                    block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
-                    key = kv[0];
-                } else {
-                    m = gmin;
-                    key = best_key(tg, gmin);
-                }
-            }
-            if (phase == 0 && m == INT32_MAX) { end_phase(); continue; }   // X == D
-            const bool best_upd = E + gmin < ebest;
-            if (best_upd) set_best(use_g ? key : best_key(tg, gmin), gmin);
-            if (phase == 1 && gmin >= 0) { end_phase(); continue; }       // R-4
-            si = key >> 1; sx = key & 1; sv = m;
-        } else if (algo == ALG_TWO) {
-            // TwoNeighbor (R-10): 0, then (k, k-1) for k = 1..n-1
-            if (q == 2 * n - 1) { end_phase(); continue; }
-            const int i = q == 0 ? 0 : ((q & 1) ? (q + 1) >> 1 : (q >> 1) - 1);
-            q++;
-            int tg = INT32_MAX;
-#pragma unroll
-            for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
-            int ov = 0, ox = 0;
-            const bool own = owns(i);
-            if (__any_sync(0xffffffffu, own)) {
-                if (own) {
-                    ov = get_at(d, lbit(i));
-                    ox = (int)((xb >> lbit(i)) & 1);
-                }
-            }
-            if constexpr (MW) {
-                if (own) { bc_s[rc & 1][0] = ov; bc_s[rc & 1][1] = ox; }
-            }
-            int v[1] = {tg};
-            const int ops[1] = {OP_MIN};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            if constexpr (MW) {
-                ov = bc_s[(rc - 1) & 1][0];
-                ox = bc_s[(rc - 1) & 1][1];
-            } else {
-                const int src = (i >> 3) & 31;
-                ov = __shfl_sync(0xffffffffu, ov, src);
-                ox = __shfl_sync(0xffffffffu, ox, src);
-            }
-            const int gmin = v[0];
-            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
-            si = i; sv = ov; sx = ox;
-        } else {
-            if (tt == p.T) { end_phase(); continue; }
-            tt++;
-            const bits_t tm = tabu_mask();
-            const bits_t el = ~tm & vb;
-            int tg = INT32_MAX;
-            if (algo == ALG_MAXMIN) {
-                // MaxMin (R-6)
-                int lo = INT32_MAX, hi = INT32_MIN, hv = INT32_MIN;
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if ((el >> k) & 1) { lo = min(lo, d[k]); hi = max(hi, d[k]); }
-                    if ((vb >> k) & 1) hv = max(hv, d[k]);
-                }
-                int v[5] = {tg, lo, hi, el != 0, hv};
-                const int ops[5] = {OP_MIN, OP_MIN, OP_MAX, OP_OR, OP_MAX};
-                block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-                const int gmin = v[0];
-                const bool best_upd = E + gmin < ebest;
-                const bits_t EL = v[3] ? el : vb;
-                const int64_t LO = v[3] ? v[1] : gmin, HI = v[3] ? v[2] : v[4];
-                const uint4 r = rng4(p.seed, PUR_MAXMIN, 0, gslot, p.gen, (uint32_t)flips);
-                const uint64_t T = (uint64_t)p.T, u = (uint64_t)(p.T - tt);
-                const unsigned __int128 num = (unsigned __int128)(uint64_t)(HI - LO) * (u * u * u);
-                const uint64_t span = (uint64_t)(num / (unsigned __int128)(T * T * T));
-                const int64_t thr = LO + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32);
-                bits_t cb = 0;
-#pragma unroll
-                for (int k = 0; k < EPT; k++)
-                    if ((int64_t)d[k] <= thr) cb |= ONE << k;
-                cb &= EL;
-                int kbl = INT32_MAX;
-                if (best_upd && __any_sync(0xffffffffu, tg == gmin))
-                    if (tg == gmin) kbl = first_key_full(vb, gmin);
-                int kb;
-                locate_pick(cb, r.y, kbl, si, sv, sx, kb);
-                if (best_upd) set_best(kb, gmin);
-            } else {
-                // PositiveMin (R-9)
-                int tp = INT32_MAX, tpv = INT32_MAX;
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if (d[k] > 0) {
-                        if ((el >> k) & 1) tp = min(tp, d[k]);
-                        if ((vb >> k) & 1) tpv = min(tpv, d[k]);
-                    }
-                }
-                int v[4] = {tg, tp, el != 0, tpv};
-                const int ops[4] = {OP_MIN, OP_MIN, OP_OR, OP_MIN};
-                block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-                const int gmin = v[0];
-                const bool best_upd = E + gmin < ebest;
-                const bits_t EL = v[2] ? el : vb;
-                const int pm = v[2] ? v[1] : v[3];     // INT32_MAX = "+inf"
-                bits_t cb = 0;
-#pragma unroll
-                for (int k = 0; k < EPT; k++)
-                    if (d[k] <= pm) cb |= ONE << k;
-                cb &= EL;
-                const uint4 r = rng4(p.seed, PUR_POSMIN, 0, gslot, p.gen, (uint32_t)flips);
-                int kbl = INT32_MAX;
-                if (best_upd && __any_sync(0xffffffffu, tg == gmin))
-                    if (tg == gmin) kbl = first_key_full(vb, gmin);
-                int kb;
-                locate_pick(cb, r.x, kbl, si, sv, sx, kb);
-                if (best_upd) set_best(kb, gmin);
-            }
-        }
-
-        // ---------------- Step 3: flip bit si
-        // (every thread has passed the last exchange, so the row buffer is free)
+    // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
+    auto do_flip = [&](int si, int sv, int sx) {
+        // every thread has passed the last exchange: the row buffer is free
         if (t == 0) {
             fence_proxy_async();
-            const char* src = Wbytes + (size_t)si * (size_t)(2 * p.n_pad);
+            const char* src = reinterpret_cast<const char*>(p.W) + (size_t)si * (size_t)(2 * p.n_pad);
 #pragma unroll
             for (int qq = 0; qq < NP; qq++)
                 bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
         }
         E += sv;
-        // s_k = sigma(x_i) sigma(x_k) = -1 on these elements (Eq.(4))
-        const bits_t negm = sx ? ~xb : xb;
-        if (__any_sync(0xffffffffu, owns(si))) {
+        const bits_t negm = sx ? ~xb : xb;   // s_k = sigma(x_i) sigma(x_k) = -1 here
+        if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
                 const int k = lbit(si);
-                neg_at(d, k);                  // Eq.(5)
+                neg_at(d, k);                    // Eq.(5)
                 xb ^= ONE << k;
                 bdiff ^= ONE << k;
             }
@@ -722,7 +403,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             if (t == 0 && s == p.trace_slot && flips < p.tr_cap) {
                 p.tr_bit[flips] = si;
                 p.tr_E[flips] = E;
-                p.tr_phase[flips] = (int8_t)(phase == 2 ? 2 + min(round, 100) : phase);
+                p.tr_phase[flips] = (int8_t)phase_code;
             }
         }
         flips++;
@@ -741,13 +422,385 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                     const int lo = (int)(int16_t)(wv[h] & 0xFFFFu);
                     const int hi = (int)wv[h] >> 16;
                     const int k0 = 8 * c + 2 * h, k1 = k0 + 1;
-                    d[k0] += ((negm >> k0) & 1) ? -lo : lo;
+                    d[k0] += ((negm >> k0) & 1) ? -lo : lo;   // Eq.(4)
                     d[k1] += ((negm >> k1) & 1) ? -hi : hi;
                 }
             }
         }
         par_row ^= 1u;
-    }
+    };
+
+    // ---------------- tabu mask (R-11): bits of the last `tabu` flips
+    auto tabu_full = [&]() -> bits_t {
+        bits_t m = 0;
+        for (int j = 0; j < tabu; j++) {
+            const int r = ring_s[(pos + j) & (TABU_RING - 1)];
+            if (r >= 0 && owns(r)) m |= ONE << lbit(r);
+        }
+        return m;
+    };
+    // after a flip: the new flip enters, the (tabu+1)-th most recent leaves
+    auto tabu_step = [&](bits_t& tm, int si) {
+        if (tabu == 0) return;
+        if (owns(si)) tm |= ONE << lbit(si);
+        const int r = ring_s[(pos + tabu) & (TABU_RING - 1)];
+        if (r >= 0 && owns(r)) {
+            bool still = false;
+            for (int j = 0; j < tabu; j++) still |= ring_s[(pos + j) & (TABU_RING - 1)] == r;
+            if (!still) tm &= ~(ONE << lbit(r));
+        }
+    };
+
+    // ---------------- phases
+    // Straight (R-5): argmin over bits with x != d until X == D
+    auto run_straight = [&]() {
+        phase_code = 0;
+        while (true) {
+            const bits_t cm = (xb ^ db) & vb;
+            const int tg = scan_min();
+            int gm[C];
+            int t1 = INT32_MAX;
+#pragma unroll
+            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
+            if (__any_sync(FULL, cm != 0)) t1 = scan_chunks_masked(cm, gm);
+            int m, key, gmin;
+            argmin_exchange(t1, gm, cm, tg, m, key, gmin);
+            if (m == INT32_MAX) return;                         // X == D
+            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
+            do_flip(key >> 1, m, key & 1);
+        }
+    };
+    // Greedy (R-4): argmin over all bits while min < 0
+    auto run_greedy = [&]() {
+        phase_code = 1;
+        while (true) {
+            int gm[C];
+            const int tg = scan_chunks(gm);
+            int m, key, gmin;
+            argmin_exchange(tg, gm, ~(bits_t)0, tg, m, key, gmin);
+            if (E + gmin < ebest) set_best(key, gmin);
+            if (gmin >= 0) return;
+            do_flip(key >> 1, gmin, key & 1);
+        }
+    };
+    // CyclicMin (R-7)
+    auto run_cyclic = [&]() {
+        bits_t tm = tabu_full();
+        int cursor = 0;
+        for (int tt = 1; tt <= p.T; tt++) {
+            const int w = p.wtab[tt];
+            const int b0 = min(cursor + w, n), b1 = cursor + w - n;
+            bits_t wm = 0;
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                const int base = gidx(c, 0);
+                const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
+                if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
+                const int hi2 = min(b1 - base, 8);
+                if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
+            }
+            cursor = (cursor + w) % n;
+            const bits_t M1 = wm & ~tm;
+            const int tg = scan_min();
+            int gm[C];
+            int t1 = INT32_MAX;
+#pragma unroll
+            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
+            if (__any_sync(FULL, M1 != 0)) t1 = scan_chunks_masked(M1, gm);
+            int m, key, gmin;
+            argmin_exchange(t1, gm, M1, tg, m, key, gmin);
+            if (m == INT32_MAX) argmin_slow(wm, m, key);      // window all tabu: drop tabu
+            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
+            const int si = key >> 1;
+            do_flip(si, m, key & 1);
+            tabu_step(tm, si);
+        }
+    };
+    // RandomMin (R-8)
+    auto run_random = [&]() {
+        bits_t tm = tabu_full();
+        for (int tt = 1; tt <= p.T; tt++) {
+            const uint32_t p16 = (uint32_t)p.ptab[tt];
+            bits_t cand;
+            if (p16 >= 65536u) {
+                cand = vb;
+            } else {
+                cand = 0;
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot, p.gen,
+                                         (uint32_t)flips);
+                    const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
+                    uint32_t byte = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const uint32_t u16 = (wds[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+                        byte |= (uint32_t)(u16 < p16) << e;
+                    }
+                    cand |= (bits_t)byte << (8 * c);
+                }
+            }
+            const bits_t M1 = cand & ~tm & vb;
+            const int tg = scan_min();
+            int gm[C];
+            int t1 = INT32_MAX;
+#pragma unroll
+            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
+            if (__any_sync(FULL, M1 != 0)) t1 = scan_chunks_masked(M1, gm);
+            int m, key, gmin;
+            argmin_exchange(t1, gm, M1, tg, m, key, gmin);
+            if (m == INT32_MAX) {                               // no candidate (R-8)
+                argmin_slow(~tm & vb, m, key);
+                if (m == INT32_MAX) { m = gmin; key = best_key(tg, gmin); }   // all tabu (R-11)
+            }
+            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
+            const int si = key >> 1;
+            do_flip(si, m, key & 1);
+            tabu_step(tm, si);
+        }
+    };
+
+    // count + uniform pick in index order (MaxMin R-6, PositiveMin R-9):
+    // picks the floor(u |C| / 2^32)-th member of cb in ascending index order.
+    auto locate_pick = [&](bits_t cb, uint32_t u, int& si, int& sv, int& sx) {
+        int incl[C];   // warp-inclusive prefix of this lane's candidate count, per chunk
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            int x = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(FULL, x, off);
+                if (lane >= off) x += y;
+            }
+            incl[c] = x;
+        }
+        int par = 0;
+        if constexpr (MW) {
+            par = rc & 1;
+            rc++;
+            if (lane == 31) {
+#pragma unroll
+                for (int c = 0; c < C; c++) red_s[par][wid][c] = incl[c];
+            }
+            __syncthreads();
+        }
+        // chunk-major order: all of chunk 0 (thread order), then chunk 1, ...
+        int tot = 0;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            int woff = 0, Tc;
+            if constexpr (MW) {
+                const int x = lane < NW ? red_s[par][lane][c] : 0;
+                int y = x;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int z = __shfl_up_sync(FULL, y, off);
+                    if (lane >= off) y += z;
+                }
+                woff = __shfl_sync(FULL, y - x, wid);
+                Tc = __shfl_sync(FULL, y, 31);
+            } else {
+                Tc = __shfl_sync(FULL, incl[c], 31);
+            }
+            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
+            incl[c] = tot + woff + incl[c] - cnt;   // rank of this lane's first candidate in chunk c
+            tot += Tc;
+        }
+        const int r = (int)pick_u(u, (uint32_t)tot);
+        int li = -1;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
+            const int lo = incl[c];
+            if (r >= lo && r < lo + cnt) {
+                uint32_t byte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
+                for (int j = 0; j < r - lo; j++) byte &= byte - 1;   // drop lower set bits
+                li = 8 * c + (__ffs(byte) - 1);
+            }
+        }
+        int gi = -1, lv = 0, lx = 0;
+        if (__any_sync(FULL, li >= 0)) {
+            if (li >= 0) {
+                gi = gidx(li >> 3, li & 7);
+                lv = get_at(d, li);
+                lx = (int)((xb >> li) & 1);
+            }
+        }
+        if constexpr (MW) {
+            const int par2 = rc & 1;
+            rc++;
+            if (li >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
+            __syncthreads();
+            si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
+        } else {
+            const int src = __ffs(__ballot_sync(FULL, li >= 0)) - 1;
+            si = __shfl_sync(FULL, gi, src);
+            sv = __shfl_sync(FULL, lv, src);
+            sx = __shfl_sync(FULL, lx, src);
+        }
+    };
+
+    // MaxMin (R-6)
+    auto run_maxmin = [&]() {
+        bits_t tm = tabu_full();
+        for (int tt = 1; tt <= p.T; tt++) {
+            const bits_t el = ~tm & vb;
+            int tg = INT32_MAX, lo = INT32_MAX, hi = INT32_MIN;
+            if (__any_sync(FULL, el != ~(bits_t)0)) {   // lanes with tabu bits or pads: masked
+#pragma unroll
+                for (int k = 0; k < EPT; k++) {
+                    tg = min(tg, d[k]);
+                    if ((el >> k) & 1) { lo = min(lo, d[k]); hi = max(hi, d[k]); }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < EPT; k++) {
+                    tg = min(tg, d[k]);
+                    hi = max(hi, d[k]);
+                }
+                lo = tg;
+            }
+            int v[4] = {tg, lo, hi, el != 0};
+            const int ops[4] = {OP_MIN, OP_MIN, OP_MAX, OP_OR};
+            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            const int gmin = v[0];
+            bits_t EL = el;
+            int64_t LO = v[1], HI = v[2];
+            if (!v[3]) {                                // every bit tabu: drop tabu (R-11)
+                EL = vb;
+                int hv = INT32_MIN;
+#pragma unroll
+                for (int k = 0; k < EPT; k++)
+                    if ((vb >> k) & 1) hv = max(hv, d[k]);
+                int v2[1] = {hv};
+                const int ops2[1] = {OP_MAX};
+                block_reduce<MW>(v2, ops2, red_s, rc, lane, wid, NW);
+                LO = gmin;
+                HI = v2[0];
+            }
+            const uint4 r = rng4(p.seed, PUR_MAXMIN, 0, gslot, p.gen, (uint32_t)flips);
+            const uint64_t T = (uint64_t)p.T, u = (uint64_t)(p.T - tt);
+            const unsigned __int128 num = (unsigned __int128)(uint64_t)(HI - LO) * (u * u * u);
+            const uint64_t span = (uint64_t)(num / (unsigned __int128)(T * T * T));
+            const int thr = (int)(LO + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32));
+            bits_t cb = 0;
+#pragma unroll
+            for (int k = 0; k < EPT; k++)
+                if (d[k] <= thr) cb |= ONE << k;
+            cb &= EL;
+            const bool bu = E + gmin < ebest;
+            int bk = INT32_MAX;
+            if (bu) bk = best_key(tg, gmin);
+            int si, sv, sx;
+            locate_pick(cb, r.y, si, sv, sx);
+            if (bu) set_best(bk, gmin);
+            do_flip(si, sv, sx);
+            tabu_step(tm, si);
+        }
+    };
+    // PositiveMin (R-9)
+    auto run_posmin = [&]() {
+        bits_t tm = tabu_full();
+        for (int tt = 1; tt <= p.T; tt++) {
+            const bits_t el = ~tm & vb;
+            int tg = INT32_MAX;
+            unsigned tp = 0xFFFFFFFFu;   // min over eligible positive Delta, as Delta-1 unsigned
+            if (__any_sync(FULL, (el | ~vb) != ~(bits_t)0)) {   // lanes with tabu bits
+#pragma unroll
+                for (int k = 0; k < EPT; k++) {
+                    tg = min(tg, d[k]);
+                    if ((el >> k) & 1) tp = min(tp, (unsigned)(d[k] - 1));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < EPT; k++) {
+                    tg = min(tg, d[k]);
+                    tp = min(tp, (unsigned)(d[k] - 1));   // pads (INT32_MAX) never win
+                }
+            }
+            // Delta <= 0 maps to >= 2^31 - 1 (as unsigned); keep only real positives
+            int tpi = tp < 0x7FFFFFFEu ? (int)tp + 1 : INT32_MAX;
+            int v[3] = {tg, tpi, el != 0};
+            const int ops[3] = {OP_MIN, OP_MIN, OP_OR};
+            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            const int gmin = v[0];
+            bits_t EL = el;
+            int pm = v[1];                              // INT32_MAX = "+inf"
+            if (!v[2]) {                                // every bit tabu (R-11)
+                EL = vb;
+                unsigned t2 = 0xFFFFFFFFu;
+#pragma unroll
+                for (int k = 0; k < EPT; k++) t2 = min(t2, (unsigned)(d[k] - 1));
+                int v2[1] = {t2 < 0x7FFFFFFEu ? (int)t2 + 1 : INT32_MAX};
+                const int ops2[1] = {OP_MIN};
+                block_reduce<MW>(v2, ops2, red_s, rc, lane, wid, NW);
+                pm = v2[0];
+            }
+            bits_t cb = 0;
+#pragma unroll
+            for (int k = 0; k < EPT; k++)
+                if (d[k] <= pm) cb |= ONE << k;
+            cb &= EL;
+            const uint4 r = rng4(p.seed, PUR_POSMIN, 0, gslot, p.gen, (uint32_t)flips);
+            const bool bu = E + gmin < ebest;
+            int bk = INT32_MAX;
+            if (bu) bk = best_key(tg, gmin);
+            int si, sv, sx;
+            locate_pick(cb, r.x, si, sv, sx);
+            if (bu) set_best(bk, gmin);
+            do_flip(si, sv, sx);
+            tabu_step(tm, si);
+        }
+    };
+    // TwoNeighbor (R-10): 0, then (k, k-1) for k = 1..n-1
+    auto run_two = [&]() {
+        for (int q = 0; q < 2 * n - 1; q++) {
+            const int i = q == 0 ? 0 : ((q & 1) ? (q + 1) >> 1 : (q >> 1) - 1);
+            const int tg = scan_min();
+            int ov = 0, ox = 0;
+            const bool own = owns(i);
+            if (__any_sync(FULL, own)) {
+                if (own) {
+                    ov = get_at(d, lbit(i));
+                    ox = (int)((xb >> lbit(i)) & 1);
+                }
+            }
+            if constexpr (MW) {
+                if (own) { bc_s[rc & 1][0] = ov; bc_s[rc & 1][1] = ox; }
+            }
+            int v[1] = {tg};
+            const int ops[1] = {OP_MIN};
+            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            if constexpr (MW) {
+                ov = bc_s[(rc - 1) & 1][0];
+                ox = bc_s[(rc - 1) & 1][1];
+            } else {
+                const int src = (i >> 3) & 31;
+                ov = __shfl_sync(FULL, ov, src);
+                ox = __shfl_sync(FULL, ox, src);
+            }
+            const int gmin = v[0];
+            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
+            do_flip(i, ov, ox);
+        }
+    };
+
+    // ---------------- batch control (R-12)
+    run_straight();
+    run_greedy();
+    int round = 0;
+    do {
+        phase_code = 2 + min(round, 100);
+        switch (algo) {
+        case ALG_MAXMIN: run_maxmin(); break;
+        case ALG_CYCLIC: run_cyclic(); break;
+        case ALG_RANDOM: run_random(); break;
+        case ALG_POSMIN: run_posmin(); break;
+        default: run_two(); break;
+        }
+        run_greedy();
+        round++;
+    } while (algo != ALG_TWO && flips < p.B);
 
     // ---------------- write back state and the result packet
     {
