@@ -196,14 +196,27 @@ __device__ __forceinline__ int first_in_chunk(const int32_t (&d)[EPT], bits_t M,
     return r;
 }
 
+// floor(a * f / q) exactly, a < 2^33, f, q <= 2^48 (MaxMin span, R-6):
+// a double estimate corrected with 128-bit integer products.
+__device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_t q)
+{
+    const unsigned __int128 num = (unsigned __int128)a * f;
+    uint64_t est = (uint64_t)((double)a * (double)f / (double)q);
+    while ((unsigned __int128)est * q > num) est--;
+    while ((unsigned __int128)(est + 1) * q <= num) est++;
+    return est;
+}
+
 template <int C, bool MW, bool TRACE>
 __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams p)
 {
     constexpr int EPT = 8 * C;
     constexpr int NP = MW ? (C >= 4 ? 4 : C) : 1;   // row pieces, one mbarrier each
     constexpr int CPP = C / NP;                      // chunks per piece
+    constexpr int CW = (C + 1) / 2;                  // packed count words (two 16-bit fields)
     using bits_t = typename std::conditional<(EPT > 32), unsigned long long, uint32_t>::type;
     constexpr bits_t ONE = 1;
+    constexpr bits_t ALL = ~(bits_t)0;
     constexpr unsigned FULL = 0xffffffffu;
     const int t = threadIdx.x;
     const int NT = MW ? (int)blockDim.x : 32;
@@ -250,135 +263,420 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     int64_t E = p.E[s];
     const int algo = p.algo[s];
     const int tabu = p.tabu;
+    const int T = p.T;
     const uint32_t piece_bytes = (uint32_t)(2 * p.n_pad / NP);
     uint32_t par_row = 0;
     int flips = 0;
     int64_t ebest = E_INF;
     bits_t bdiff = 0;              // BEST = X xor bdiff
     int rc = 0;                    // exchange parity counter
-    int phase_code = 0;            // for the trace: 0 Straight, 1 Greedy, 2+r main round r
     if constexpr (MW) __syncthreads(); else __syncwarp();
 
     auto gidx = [&](int c, int e) { return (((c << lgNT) + t) << 3) | e; };
     auto owns = [&](int k) { return ((k >> 3) & (NT - 1)) == t; };
     auto lbit = [&](int k) { return (((k >> 3) >> lgNT) << 3) | (k & 7); };
 
-    // ---------------- scans (Step 1 and the argmin rules of Step 2)
-    auto scan_min = [&]() -> int {            // min over all elements (pads are INT32_MAX)
-        int m = INT32_MAX;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) m = min(m, d[k]);
-        return m;
-    };
-    auto scan_chunks = [&](int (&gm)[C]) -> int {   // per-chunk minima, all elements
-        int m = INT32_MAX;
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            int mc = INT32_MAX;
-#pragma unroll
-            for (int e = 0; e < 8; e++) mc = min(mc, d[8 * c + e]);
-            gm[c] = mc;
-            m = min(m, mc);
+    // phases: 0 Straight, 1 Greedy, 2 main (R-12)
+    int phase = 0, round = 0, tt = 0, cursor = 0;
+    bool after_main = false;
+    bits_t tm = 0;                 // tabu mask of this thread's elements (main phases, R-11)
+
+    while (true) {
+        // ---------------- phase transitions
+        if (phase == 2 && tt == (algo == ALG_TWO ? 2 * n - 1 : T)) {
+            phase = 1;
+            after_main = true;
         }
-        return m;
-    };
-    auto scan_chunks_masked = [&](bits_t M, int (&gm)[C]) -> int {   // per-chunk minima over M
-        int m = INT32_MAX;
+        // ---------------- Step 2 setup: candidate masks (uniform control)
+        // kind 0: argmin over M1 (masked) or over all bits (!masked)
+        // kind 1: uniform pick among candidates (MaxMin, PositiveMin)
+        // kind 2: fixed bit (TwoNeighbor)
+        int kind = 0;
+        bool masked = true;
+        bits_t M1 = vb, M2 = 0;
+        int fb = 0;                    // fallback: 1 drop tabu in the window, 2 RandomMin
+        int fixed_i = 0;
+        if (phase == 0) {
+            M1 = (xb ^ db) & vb;                                   // Straight
+        } else if (phase == 1) {
+            masked = false;                                        // Greedy
+        } else {
+            tt++;
+            if (tt == 1) {                                         // main run starts
+                cursor = 0;
+                tm = 0;
+                if (algo != ALG_TWO)
+                    for (int j = 0; j < tabu; j++) {
+                        const int r = ring_s[(pos + j) & (TABU_RING - 1)];
+                        if (r >= 0 && owns(r)) tm |= ONE << lbit(r);
+                    }
+            }
+            if (algo == ALG_CYCLIC) {                              // CyclicMin (R-7)
+                const int w = p.wtab[tt];
+                const int b0 = min(cursor + w, n), b1 = cursor + w - n;
+                bits_t wm = 0;
 #pragma unroll
-        for (int c = 0; c < C; c++) {
-            int mc = INT32_MAX;
-#pragma unroll
-            for (int e = 0; e < 8; e++)
-                if ((M >> (8 * c + e)) & 1) mc = min(mc, d[8 * c + e]);
-            gm[c] = mc;
-            m = min(m, mc);
-        }
-        return m;
-    };
-    // lowest (index<<1 | x) among this thread's elements in M with d == m (full scan; rare use)
-    auto first_key_full = [&](bits_t M, int m) -> int {
-        int key = INT32_MAX;
-#pragma unroll
-        for (int c = C - 1; c >= 0; c--) {
-#pragma unroll
-            for (int e = 7; e >= 0; e--) {
-                const int k = 8 * c + e;
-                if (((M >> k) & 1) && d[k] == m) key = (gidx(c, e) << 1) | (int)((xb >> k) & 1);
+                for (int c = 0; c < C; c++) {
+                    const int base = gidx(c, 0);
+                    const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
+                    if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
+                    const int hi2 = min(b1 - base, 8);
+                    if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
+                }
+                cursor = (cursor + w) % n;
+                M1 = wm & ~tm;
+                M2 = wm;
+                fb = 1;
+            } else if (algo == ALG_RANDOM) {                       // RandomMin (R-8)
+                const uint32_t p16 = (uint32_t)p.ptab[tt];
+                bits_t cand = vb;
+                if (p16 < 65536u) {
+                    cand = 0;
+#pragma unroll 1
+                    for (int c = 0; c < C; c++) {
+                        const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot, p.gen,
+                                             (uint32_t)flips);
+                        uint32_t byte = (uint32_t)((r.x & 0xFFFFu) < p16) | ((uint32_t)((r.x >> 16) < p16) << 1) |
+                                        ((uint32_t)((r.y & 0xFFFFu) < p16) << 2) | ((uint32_t)((r.y >> 16) < p16) << 3) |
+                                        ((uint32_t)((r.z & 0xFFFFu) < p16) << 4) | ((uint32_t)((r.z >> 16) < p16) << 5) |
+                                        ((uint32_t)((r.w & 0xFFFFu) < p16) << 6) | ((uint32_t)((r.w >> 16) < p16) << 7);
+                        cand |= (bits_t)byte << (8 * c);
+                    }
+                }
+                M1 = cand & ~tm & vb;
+                M2 = ~tm & vb;
+                fb = 2;
+            } else if (algo == ALG_TWO) {                          // TwoNeighbor (R-10)
+                kind = 2;
+                const int q = tt - 1;
+                fixed_i = q == 0 ? 0 : ((q & 1) ? (q + 1) >> 1 : (q >> 1) - 1);
+            } else {
+                kind = 1;                                          // MaxMin / PositiveMin
             }
         }
-        return key;
-    };
-    // key of the first element with value m, from per-chunk minima (one lane runs it)
-    auto key_from_chunks = [&](const int (&gm)[C], bits_t M, int m) -> int {
-        int cs = 0;
-#pragma unroll
-        for (int c = C - 1; c >= 0; c--)
-            if (gm[c] == m) cs = c;
-        const int e = first_in_chunk(d, M, cs, m);
-        const int k = 8 * cs + e;
-        return (gidx(cs, e) << 1) | (int)((xb >> k) & 1);
-    };
-    // One exchange: argmin (value, lowest key) of the rule + min of tg (Step 1).
-    auto argmin_exchange = [&](int tsel, const int (&gm)[C], bits_t M, int tg, int& m, int& key,
-                               int& gmin) {
-        const int wmin = warp_min(tsel);
-        int k = INT32_MAX;
-        if (__any_sync(FULL, tsel == wmin && wmin != INT32_MAX))
-            if (tsel == wmin && wmin != INT32_MAX) k = key_from_chunks(gm, M, wmin);
-        k = warp_min(k);
-        int g = warp_min(tg);
-        if constexpr (MW) {
-            const int par = rc & 1;
-            rc++;
-            if (lane == 0) { red_s[par][wid][0] = wmin; red_s[par][wid][1] = k; red_s[par][wid][2] = g; }
-            __syncthreads();
-            const int a = lane < NW ? red_s[par][lane][0] : INT32_MAX;
-            const int b = lane < NW ? red_s[par][lane][1] : INT32_MAX;
-            const int c = lane < NW ? red_s[par][lane][2] : INT32_MAX;
-            m = warp_min(a);
-            key = warp_min(a == m ? b : INT32_MAX);
-            gmin = warp_min(c);
-        } else {
-            m = wmin;
-            key = k;
-            gmin = g;
-        }
-    };
-    // lazy key of the global-min element (BEST update, rare)
-    auto best_key = [&](int tg, int gmin) -> int {
-        int k = INT32_MAX;
-        if (__any_sync(FULL, tg == gmin))
-            if (tg == gmin) k = first_key_full(vb, gmin);
-        int v[1] = {k};
-        const int ops[1] = {OP_MIN};
-        block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-        return v[0];
-    };
-    // masked argmin over M with a full-scan key (fallback paths, rare)
-    auto argmin_slow = [&](bits_t M, int& m, int& key) {
-        int tm_ = INT32_MAX;
-#pragma unroll
-        for (int k = 0; k < EPT; k++)
-            if ((M >> k) & 1) tm_ = min(tm_, d[k]);
-        int v[1] = {tm_};
-        const int ops[1] = {OP_MIN};
-        block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-        m = v[0];
-        int kk = INT32_MAX;
-        if (__any_sync(FULL, tm_ == m && m != INT32_MAX))
-            if (tm_ == m && m != INT32_MAX) kk = first_key_full(M, m);
-        int kv[1] = {kk};
-        block_reduce<MW>(kv, ops, red_s, rc, lane, wid, NW);
-        key = kv[0];
-    };
-    auto set_best = [&](int key, int m) {
-        ebest = E + m;
-        const int j = key >> 1;
-        bdiff = owns(j) ? (ONE << lbit(j)) : (bits_t)0;
-    };
 
-    // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
-    auto do_flip = [&](int si, int sv, int sx) {
+        // ---------------- Step 1 + Step 2: scans and one exchange
+        int si = 0, sv = 0, sx = 0;     // selected bit, its Delta, its x (uniform)
+        int gmin = 0, tg = INT32_MAX;
+        int key = INT32_MAX;            // argmin key of the rule (kind 0)
+        if (kind == 0) {
+            int gm[C];
+            int tsel = INT32_MAX;
+            if (!masked) {
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    int mc = INT32_MAX;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) mc = min(mc, d[8 * c + e]);
+                    gm[c] = mc;
+                    tg = min(tg, mc);
+                }
+                tsel = tg;
+                M1 = ALL;
+            } else {
+#pragma unroll
+                for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
+#pragma unroll
+                for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
+                if (__any_sync(FULL, M1 != 0)) {      // warps without candidates skip
+#pragma unroll
+                    for (int c = 0; c < C; c++) {
+                        int mc = INT32_MAX;
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            if ((M1 >> (8 * c + e)) & 1) mc = min(mc, d[8 * c + e]);
+                        gm[c] = mc;
+                        tsel = min(tsel, mc);
+                    }
+                }
+            }
+            // warp argmin with a lazy key: only the lane(s) holding the minimum search
+            const int wmin = warp_min(tsel);
+            int k = INT32_MAX;
+            if (__any_sync(FULL, tsel == wmin && wmin != INT32_MAX)) {
+                if (tsel == wmin && wmin != INT32_MAX) {
+                    int cs = 0;
+#pragma unroll
+                    for (int c = C - 1; c >= 0; c--)
+                        if (gm[c] == wmin) cs = c;
+                    const int e = first_in_chunk(d, M1, cs, wmin);
+                    k = (gidx(cs, e) << 1) | (int)((xb >> (8 * cs + e)) & 1);
+                }
+            }
+            k = warp_min(k);
+            int g = warp_min(tg);
+            int m;
+            if constexpr (MW) {
+                const int par = rc & 1;
+                rc++;
+                if (lane == 0) { red_s[par][wid][0] = wmin; red_s[par][wid][1] = k; red_s[par][wid][2] = g; }
+                __syncthreads();
+                const int a = lane < NW ? red_s[par][lane][0] : INT32_MAX;
+                const int b = lane < NW ? red_s[par][lane][1] : INT32_MAX;
+                const int c2 = lane < NW ? red_s[par][lane][2] : INT32_MAX;
+                m = warp_min(a);
+                key = warp_min(a == m ? b : INT32_MAX);
+                gmin = warp_min(c2);
+            } else {
+                m = wmin;
+                key = k;
+                gmin = g;
+            }
+            if (m == INT32_MAX) {
+                if (phase == 0) {                   // X == D: Straight ends (no scan, R-3)
+                    phase = 1;
+                    after_main = false;
+                    continue;
+                }
+                // empty candidate set (R-7, R-8, R-11): argmin over M2, then over all bits
+                int t2 = INT32_MAX;
+#pragma unroll
+                for (int kk = 0; kk < EPT; kk++)
+                    if ((M2 >> kk) & 1) t2 = min(t2, d[kk]);
+                int v2[1] = {t2};
+                const int ops1[1] = {OP_MIN};
+                block_reduce<MW>(v2, ops1, red_s, rc, lane, wid, NW);
+                bits_t MM = M2;
+                if (v2[0] == INT32_MAX) { MM = vb; t2 = tg; v2[0] = gmin; }
+                m = v2[0];
+                int k2 = INT32_MAX;
+                if (__any_sync(FULL, t2 == m))
+                    if (t2 == m) {
+#pragma unroll
+                        for (int c = C - 1; c >= 0; c--)
+#pragma unroll
+                            for (int e = 7; e >= 0; e--) {
+                                const int kk = 8 * c + e;
+                                if (((MM >> kk) & 1) && d[kk] == m) k2 = (gidx(c, e) << 1) | (int)((xb >> kk) & 1);
+                            }
+                    }
+                int kv[1] = {k2};
+                block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
+                key = kv[0];
+            }
+            si = key >> 1;
+            sx = key & 1;
+            sv = m;
+        } else if (kind == 2) {
+            // TwoNeighbor: scan, and the owner of fixed_i publishes Delta_i and x_i
+#pragma unroll
+            for (int kk = 0; kk < EPT; kk++) tg = min(tg, d[kk]);
+            int ov = 0, ox = 0;
+            const bool own = owns(fixed_i);
+            if (__any_sync(FULL, own)) {
+                if (own) {
+                    ov = get_at(d, lbit(fixed_i));
+                    ox = (int)((xb >> lbit(fixed_i)) & 1);
+                }
+            }
+            if constexpr (MW) {
+                if (own) { bc_s[rc & 1][0] = ov; bc_s[rc & 1][1] = ox; }
+            }
+            int v[1] = {tg};
+            const int ops[1] = {OP_MIN};
+            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            if constexpr (MW) {
+                ov = bc_s[(rc - 1) & 1][0];
+                ox = bc_s[(rc - 1) & 1][1];
+            } else {
+                const int src = (fixed_i >> 3) & 31;
+                ov = __shfl_sync(FULL, ov, src);
+                ox = __shfl_sync(FULL, ox, src);
+            }
+            gmin = v[0];
+            si = fixed_i; sv = ov; sx = ox;
+        } else {
+            // MaxMin (R-6) / PositiveMin (R-9)
+            const bits_t el = ~tm & vb;
+            const bool lane_plain = (el == ALL);        // no tabu bit, no padding in this lane
+            int a1 = INT32_MAX, a2 = INT32_MIN;         // MaxMin: lo, hi; PositiveMin: pm, unused
+            if (algo == ALG_MAXMIN) {
+                if (__all_sync(FULL, lane_plain)) {
+#pragma unroll
+                    for (int kk = 0; kk < EPT; kk++) { tg = min(tg, d[kk]); a2 = max(a2, d[kk]); }
+                    a1 = tg;
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < EPT; kk++) {
+                        tg = min(tg, d[kk]);
+                        if ((el >> kk) & 1) { a1 = min(a1, d[kk]); a2 = max(a2, d[kk]); }
+                    }
+                }
+            } else {
+                unsigned tp = 0xFFFFFFFFu;   // min over eligible positive Delta as (Delta - 1), unsigned
+                if (__all_sync(FULL, (el | ~vb) == ALL)) {
+#pragma unroll
+                    for (int kk = 0; kk < EPT; kk++) { tg = min(tg, d[kk]); tp = min(tp, (unsigned)(d[kk] - 1)); }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < EPT; kk++) {
+                        tg = min(tg, d[kk]);
+                        if ((el >> kk) & 1) tp = min(tp, (unsigned)(d[kk] - 1));
+                    }
+                }
+                a1 = tp < 0x7FFFFFFEu ? (int)tp + 1 : INT32_MAX;   // pads / non-positive never count
+            }
+            int v[4] = {tg, a1, a2, el != 0};
+            const int ops[4] = {OP_MIN, OP_MIN, OP_MAX, OP_OR};
+            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            gmin = v[0];
+            bits_t EL = el;
+            int thr;
+            const uint4 r = rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
+                                 (uint32_t)flips);
+            if (!v[3]) {
+                // every bit tabu: drop tabu (R-11)
+                EL = vb;
+                int b1 = INT32_MIN;
+                unsigned b2 = 0xFFFFFFFFu;
+#pragma unroll
+                for (int kk = 0; kk < EPT; kk++)
+                    if ((vb >> kk) & 1) { b1 = max(b1, d[kk]); b2 = min(b2, (unsigned)(d[kk] - 1)); }
+                int w2[2] = {b1, b2 < 0x7FFFFFFEu ? (int)b2 + 1 : INT32_MAX};
+                const int ops2[2] = {OP_MAX, OP_MIN};
+                block_reduce<MW>(w2, ops2, red_s, rc, lane, wid, NW);
+                v[1] = algo == ALG_MAXMIN ? gmin : w2[1];
+                v[2] = w2[0];
+            }
+            uint32_t u;
+            if (algo == ALG_MAXMIN) {
+                const uint64_t uu = (uint64_t)(T - tt);
+                const uint64_t span = muldiv_floor((uint64_t)((int64_t)v[2] - v[1]), uu * uu * uu,
+                                                   (uint64_t)T * T * T);
+                thr = (int)((int64_t)v[1] + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32));
+                u = r.y;
+            } else {
+                thr = v[1];                               // INT32_MAX = "+inf": all eligible
+                u = r.x;
+            }
+            // count candidates (Delta <= thr, eligible) per chunk, packed 2 x 16 bits per word
+            uint32_t pk[CW];
+#pragma unroll
+            for (int w = 0; w < CW; w++) pk[w] = 0;
+            bits_t cb = 0;
+#pragma unroll
+            for (int kk = 0; kk < EPT; kk++)
+                if (d[kk] <= thr) cb |= ONE << kk;
+            cb &= EL;
+#pragma unroll
+            for (int c = 0; c < C; c++)
+                pk[c >> 1] += (uint32_t)__popc((uint32_t)((cb >> (8 * c)) & 0xFFu)) << (16 * (c & 1));
+            uint32_t wt[CW];
+#pragma unroll
+            for (int w = 0; w < CW; w++) wt[w] = warp_add(pk[w]);
+            uint32_t bt[CW];
+            int par = 0;
+            if constexpr (MW) {
+                par = rc & 1;
+                rc++;
+                if (lane == 0) {
+#pragma unroll
+                    for (int w = 0; w < CW; w++) red_s[par][wid][w] = (int)wt[w];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int w = 0; w < CW; w++) bt[w] = warp_add(lane < NW ? (uint32_t)red_s[par][lane][w] : 0u);
+            } else {
+#pragma unroll
+                for (int w = 0; w < CW; w++) bt[w] = wt[w];
+            }
+            // chunk-major order: chunk 0 of all threads, then chunk 1, ...
+            uint32_t tot = 0;
+#pragma unroll
+            for (int c = 0; c < C; c++) tot += (bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+            int r1 = (int)pick_u(u, tot);
+            int cs = 0;
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                const int tc = (int)((bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
+                if (cs == c && r1 >= tc) { r1 -= tc; cs = c + 1; }
+            }
+            // which warp holds rank r1 of chunk cs
+            int wsel = 0;
+            if constexpr (MW) {
+                int x = lane < NW ? (int)(((uint32_t)red_s[par][lane][cs >> 1] >> (16 * (cs & 1))) & 0xFFFFu) : 0;
+                int y = x;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int z = __shfl_up_sync(FULL, y, off);
+                    if (lane >= off) y += z;
+                }
+                const unsigned bal = __ballot_sync(FULL, y > r1);
+                wsel = __ffs(bal) - 1;
+                r1 -= __shfl_sync(FULL, y - x, wsel);
+            }
+            int gi = -1, lv = 0, lx = 0;
+            if (wid == wsel) {
+                uint32_t mybyte = 0;
+#pragma unroll
+                for (int c = 0; c < C; c++)
+                    if (c == cs) mybyte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
+                const int x = __popc(mybyte);
+                int y = x;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int z = __shfl_up_sync(FULL, y, off);
+                    if (lane >= off) y += z;
+                }
+                if (r1 >= y - x && r1 < y) {
+                    uint32_t byte = mybyte;
+                    for (int j = 0; j < r1 - (y - x); j++) byte &= byte - 1;
+                    const int e = __ffs(byte) - 1;
+                    const int li = 8 * cs + e;
+                    gi = gidx(cs, e);
+                    lv = get_at(d, li);
+                    lx = (int)((xb >> li) & 1);
+                }
+            }
+            if constexpr (MW) {
+                const int par2 = rc & 1;
+                rc++;
+                if (gi >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
+                __syncthreads();
+                si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
+            } else {
+                const int src = __ffs(__ballot_sync(FULL, gi >= 0)) - 1;
+                si = __shfl_sync(FULL, gi, src);
+                sv = __shfl_sync(FULL, lv, src);
+                sx = __shfl_sync(FULL, lx, src);
+            }
+        }
+
+        // ---------------- Step 1: BEST (R-2, R-3)
+        if (E + gmin < ebest) {
+            int bk = key;
+            if (kind != 0 || masked) {
+                // key of the lowest index holding gmin (rare: BEST improves)
+                int k3 = INT32_MAX;
+                if (__any_sync(FULL, tg == gmin))
+                    if (tg == gmin) {
+#pragma unroll
+                        for (int c = C - 1; c >= 0; c--)
+#pragma unroll
+                            for (int e = 7; e >= 0; e--) {
+                                const int kk = 8 * c + e;
+                                if (d[kk] == gmin) k3 = (gidx(c, e) << 1) | (int)((xb >> kk) & 1);
+                            }
+                    }
+                int kv[1] = {k3};
+                const int ops1[1] = {OP_MIN};
+                block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
+                bk = kv[0];
+            }
+            ebest = E + gmin;
+            const int j = bk >> 1;
+            bdiff = owns(j) ? (ONE << lbit(j)) : (bits_t)0;
+        }
+        if (phase == 1 && gmin >= 0) {
+            // Greedy reached a local minimum (R-4): next round, or the batch ends (R-12)
+            if (after_main && (algo == ALG_TWO || flips >= p.B)) break;
+            if (after_main) round++;
+            phase = 2;
+            tt = 0;
+            continue;
+        }
+
+        // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
         // every thread has passed the last exchange: the row buffer is free
         if (t == 0) {
             fence_proxy_async();
@@ -391,19 +689,29 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         const bits_t negm = sx ? ~xb : xb;   // s_k = sigma(x_i) sigma(x_k) = -1 here
         if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
-                const int k = lbit(si);
-                neg_at(d, k);                    // Eq.(5)
-                xb ^= ONE << k;
-                bdiff ^= ONE << k;
+                const int kk = lbit(si);
+                neg_at(d, kk);                   // Eq.(5)
+                xb ^= ONE << kk;
+                bdiff ^= ONE << kk;
             }
         }
         pos = (pos + TABU_RING - 1) & (TABU_RING - 1);
         ring_s[pos] = si;
+        if (phase == 2 && tabu > 0 && algo != ALG_TWO) {
+            // tabu (R-11): si enters; the (tabu+1)-th most recent flip leaves
+            if (owns(si)) tm |= ONE << lbit(si);
+            const int r = ring_s[(pos + tabu) & (TABU_RING - 1)];
+            if (r >= 0 && owns(r)) {
+                bool still = false;
+                for (int j = 0; j < tabu; j++) still |= ring_s[(pos + j) & (TABU_RING - 1)] == r;
+                if (!still) tm &= ~(ONE << lbit(r));
+            }
+        }
         if constexpr (TRACE) {
             if (t == 0 && s == p.trace_slot && flips < p.tr_cap) {
                 p.tr_bit[flips] = si;
                 p.tr_E[flips] = E;
-                p.tr_phase[flips] = (int8_t)phase_code;
+                p.tr_phase[flips] = (int8_t)(phase == 2 ? 2 + min(round, 100) : phase);
             }
         }
         flips++;
@@ -428,379 +736,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             }
         }
         par_row ^= 1u;
-    };
-
-    // ---------------- tabu mask (R-11): bits of the last `tabu` flips
-    auto tabu_full = [&]() -> bits_t {
-        bits_t m = 0;
-        for (int j = 0; j < tabu; j++) {
-            const int r = ring_s[(pos + j) & (TABU_RING - 1)];
-            if (r >= 0 && owns(r)) m |= ONE << lbit(r);
-        }
-        return m;
-    };
-    // after a flip: the new flip enters, the (tabu+1)-th most recent leaves
-    auto tabu_step = [&](bits_t& tm, int si) {
-        if (tabu == 0) return;
-        if (owns(si)) tm |= ONE << lbit(si);
-        const int r = ring_s[(pos + tabu) & (TABU_RING - 1)];
-        if (r >= 0 && owns(r)) {
-            bool still = false;
-            for (int j = 0; j < tabu; j++) still |= ring_s[(pos + j) & (TABU_RING - 1)] == r;
-            if (!still) tm &= ~(ONE << lbit(r));
-        }
-    };
-
-    // ---------------- phases
-    // Straight (R-5): argmin over bits with x != d until X == D
-    auto run_straight = [&]() {
-        phase_code = 0;
-        while (true) {
-            const bits_t cm = (xb ^ db) & vb;
-            const int tg = scan_min();
-            int gm[C];
-            int t1 = INT32_MAX;
-#pragma unroll
-            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
-            if (__any_sync(FULL, cm != 0)) t1 = scan_chunks_masked(cm, gm);
-            int m, key, gmin;
-            argmin_exchange(t1, gm, cm, tg, m, key, gmin);
-            if (m == INT32_MAX) return;                         // X == D
-            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
-            do_flip(key >> 1, m, key & 1);
-        }
-    };
-    // Greedy (R-4): argmin over all bits while min < 0
-    auto run_greedy = [&]() {
-        phase_code = 1;
-        while (true) {
-            int gm[C];
-            const int tg = scan_chunks(gm);
-            int m, key, gmin;
-            argmin_exchange(tg, gm, ~(bits_t)0, tg, m, key, gmin);
-            if (E + gmin < ebest) set_best(key, gmin);
-            if (gmin >= 0) return;
-            do_flip(key >> 1, gmin, key & 1);
-        }
-    };
-    // CyclicMin (R-7)
-    auto run_cyclic = [&]() {
-        bits_t tm = tabu_full();
-        int cursor = 0;
-        for (int tt = 1; tt <= p.T; tt++) {
-            const int w = p.wtab[tt];
-            const int b0 = min(cursor + w, n), b1 = cursor + w - n;
-            bits_t wm = 0;
-#pragma unroll
-            for (int c = 0; c < C; c++) {
-                const int base = gidx(c, 0);
-                const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
-                if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
-                const int hi2 = min(b1 - base, 8);
-                if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
-            }
-            cursor = (cursor + w) % n;
-            const bits_t M1 = wm & ~tm;
-            const int tg = scan_min();
-            int gm[C];
-            int t1 = INT32_MAX;
-#pragma unroll
-            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
-            if (__any_sync(FULL, M1 != 0)) t1 = scan_chunks_masked(M1, gm);
-            int m, key, gmin;
-            argmin_exchange(t1, gm, M1, tg, m, key, gmin);
-            if (m == INT32_MAX) argmin_slow(wm, m, key);      // window all tabu: drop tabu
-            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
-            const int si = key >> 1;
-            do_flip(si, m, key & 1);
-            tabu_step(tm, si);
-        }
-    };
-    // RandomMin (R-8)
-    auto run_random = [&]() {
-        bits_t tm = tabu_full();
-        for (int tt = 1; tt <= p.T; tt++) {
-            const uint32_t p16 = (uint32_t)p.ptab[tt];
-            bits_t cand;
-            if (p16 >= 65536u) {
-                cand = vb;
-            } else {
-                cand = 0;
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot, p.gen,
-                                         (uint32_t)flips);
-                    const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
-                    uint32_t byte = 0;
-#pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        const uint32_t u16 = (wds[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-                        byte |= (uint32_t)(u16 < p16) << e;
-                    }
-                    cand |= (bits_t)byte << (8 * c);
-                }
-            }
-            const bits_t M1 = cand & ~tm & vb;
-            const int tg = scan_min();
-            int gm[C];
-            int t1 = INT32_MAX;
-#pragma unroll
-            for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
-            if (__any_sync(FULL, M1 != 0)) t1 = scan_chunks_masked(M1, gm);
-            int m, key, gmin;
-            argmin_exchange(t1, gm, M1, tg, m, key, gmin);
-            if (m == INT32_MAX) {                               // no candidate (R-8)
-                argmin_slow(~tm & vb, m, key);
-                if (m == INT32_MAX) { m = gmin; key = best_key(tg, gmin); }   // all tabu (R-11)
-            }
-            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
-            const int si = key >> 1;
-            do_flip(si, m, key & 1);
-            tabu_step(tm, si);
-        }
-    };
-
-    // count + uniform pick in index order (MaxMin R-6, PositiveMin R-9):
-    // picks the floor(u |C| / 2^32)-th member of cb in ascending index order.
-    auto locate_pick = [&](bits_t cb, uint32_t u, int& si, int& sv, int& sx) {
-        int incl[C];   // warp-inclusive prefix of this lane's candidate count, per chunk
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            int x = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(FULL, x, off);
-                if (lane >= off) x += y;
-            }
-            incl[c] = x;
-        }
-        int par = 0;
-        if constexpr (MW) {
-            par = rc & 1;
-            rc++;
-            if (lane == 31) {
-#pragma unroll
-                for (int c = 0; c < C; c++) red_s[par][wid][c] = incl[c];
-            }
-            __syncthreads();
-        }
-        // chunk-major order: all of chunk 0 (thread order), then chunk 1, ...
-        int tot = 0;
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            int woff = 0, Tc;
-            if constexpr (MW) {
-                const int x = lane < NW ? red_s[par][lane][c] : 0;
-                int y = x;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int z = __shfl_up_sync(FULL, y, off);
-                    if (lane >= off) y += z;
-                }
-                woff = __shfl_sync(FULL, y - x, wid);
-                Tc = __shfl_sync(FULL, y, 31);
-            } else {
-                Tc = __shfl_sync(FULL, incl[c], 31);
-            }
-            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-            incl[c] = tot + woff + incl[c] - cnt;   // rank of this lane's first candidate in chunk c
-            tot += Tc;
-        }
-        const int r = (int)pick_u(u, (uint32_t)tot);
-        int li = -1;
-#pragma unroll
-        for (int c = 0; c < C; c++) {
-            const int cnt = __popc((uint32_t)((cb >> (8 * c)) & 0xFFu));
-            const int lo = incl[c];
-            if (r >= lo && r < lo + cnt) {
-                uint32_t byte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
-                for (int j = 0; j < r - lo; j++) byte &= byte - 1;   // drop lower set bits
-                li = 8 * c + (__ffs(byte) - 1);
-            }
-        }
-        int gi = -1, lv = 0, lx = 0;
-        if (__any_sync(FULL, li >= 0)) {
-            if (li >= 0) {
-                gi = gidx(li >> 3, li & 7);
-                lv = get_at(d, li);
-                lx = (int)((xb >> li) & 1);
-            }
-        }
-        if constexpr (MW) {
-            const int par2 = rc & 1;
-            rc++;
-            if (li >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
-            __syncthreads();
-            si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
-        } else {
-            const int src = __ffs(__ballot_sync(FULL, li >= 0)) - 1;
-            si = __shfl_sync(FULL, gi, src);
-            sv = __shfl_sync(FULL, lv, src);
-            sx = __shfl_sync(FULL, lx, src);
-        }
-    };
-
-    // MaxMin (R-6)
-    auto run_maxmin = [&]() {
-        bits_t tm = tabu_full();
-        for (int tt = 1; tt <= p.T; tt++) {
-            const bits_t el = ~tm & vb;
-            int tg = INT32_MAX, lo = INT32_MAX, hi = INT32_MIN;
-            if (__any_sync(FULL, el != ~(bits_t)0)) {   // lanes with tabu bits or pads: masked
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if ((el >> k) & 1) { lo = min(lo, d[k]); hi = max(hi, d[k]); }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    hi = max(hi, d[k]);
-                }
-                lo = tg;
-            }
-            int v[4] = {tg, lo, hi, el != 0};
-            const int ops[4] = {OP_MIN, OP_MIN, OP_MAX, OP_OR};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            const int gmin = v[0];
-            bits_t EL = el;
-            int64_t LO = v[1], HI = v[2];
-            if (!v[3]) {                                // every bit tabu: drop tabu (R-11)
-                EL = vb;
-                int hv = INT32_MIN;
-#pragma unroll
-                for (int k = 0; k < EPT; k++)
-                    if ((vb >> k) & 1) hv = max(hv, d[k]);
-                int v2[1] = {hv};
-                const int ops2[1] = {OP_MAX};
-                block_reduce<MW>(v2, ops2, red_s, rc, lane, wid, NW);
-                LO = gmin;
-                HI = v2[0];
-            }
-            const uint4 r = rng4(p.seed, PUR_MAXMIN, 0, gslot, p.gen, (uint32_t)flips);
-            const uint64_t T = (uint64_t)p.T, u = (uint64_t)(p.T - tt);
-            const unsigned __int128 num = (unsigned __int128)(uint64_t)(HI - LO) * (u * u * u);
-            const uint64_t span = (uint64_t)(num / (unsigned __int128)(T * T * T));
-            const int thr = (int)(LO + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32));
-            bits_t cb = 0;
-#pragma unroll
-            for (int k = 0; k < EPT; k++)
-                if (d[k] <= thr) cb |= ONE << k;
-            cb &= EL;
-            const bool bu = E + gmin < ebest;
-            int bk = INT32_MAX;
-            if (bu) bk = best_key(tg, gmin);
-            int si, sv, sx;
-            locate_pick(cb, r.y, si, sv, sx);
-            if (bu) set_best(bk, gmin);
-            do_flip(si, sv, sx);
-            tabu_step(tm, si);
-        }
-    };
-    // PositiveMin (R-9)
-    auto run_posmin = [&]() {
-        bits_t tm = tabu_full();
-        for (int tt = 1; tt <= p.T; tt++) {
-            const bits_t el = ~tm & vb;
-            int tg = INT32_MAX;
-            unsigned tp = 0xFFFFFFFFu;   // min over eligible positive Delta, as Delta-1 unsigned
-            if (__any_sync(FULL, (el | ~vb) != ~(bits_t)0)) {   // lanes with tabu bits
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    if ((el >> k) & 1) tp = min(tp, (unsigned)(d[k] - 1));
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < EPT; k++) {
-                    tg = min(tg, d[k]);
-                    tp = min(tp, (unsigned)(d[k] - 1));   // pads (INT32_MAX) never win
-                }
-            }
-            // Delta <= 0 maps to >= 2^31 - 1 (as unsigned); keep only real positives
-            int tpi = tp < 0x7FFFFFFEu ? (int)tp + 1 : INT32_MAX;
-            int v[3] = {tg, tpi, el != 0};
-            const int ops[3] = {OP_MIN, OP_MIN, OP_OR};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            const int gmin = v[0];
-            bits_t EL = el;
-            int pm = v[1];                              // INT32_MAX = "+inf"
-            if (!v[2]) {                                // every bit tabu (R-11)
-                EL = vb;
-                unsigned t2 = 0xFFFFFFFFu;
-#pragma unroll
-                for (int k = 0; k < EPT; k++) t2 = min(t2, (unsigned)(d[k] - 1));
-                int v2[1] = {t2 < 0x7FFFFFFEu ? (int)t2 + 1 : INT32_MAX};
-                const int ops2[1] = {OP_MIN};
-                block_reduce<MW>(v2, ops2, red_s, rc, lane, wid, NW);
-                pm = v2[0];
-            }
-            bits_t cb = 0;
-#pragma unroll
-            for (int k = 0; k < EPT; k++)
-                if (d[k] <= pm) cb |= ONE << k;
-            cb &= EL;
-            const uint4 r = rng4(p.seed, PUR_POSMIN, 0, gslot, p.gen, (uint32_t)flips);
-            const bool bu = E + gmin < ebest;
-            int bk = INT32_MAX;
-            if (bu) bk = best_key(tg, gmin);
-            int si, sv, sx;
-            locate_pick(cb, r.x, si, sv, sx);
-            if (bu) set_best(bk, gmin);
-            do_flip(si, sv, sx);
-            tabu_step(tm, si);
-        }
-    };
-    // TwoNeighbor (R-10): 0, then (k, k-1) for k = 1..n-1
-    auto run_two = [&]() {
-        for (int q = 0; q < 2 * n - 1; q++) {
-            const int i = q == 0 ? 0 : ((q & 1) ? (q + 1) >> 1 : (q >> 1) - 1);
-            const int tg = scan_min();
-            int ov = 0, ox = 0;
-            const bool own = owns(i);
-            if (__any_sync(FULL, own)) {
-                if (own) {
-                    ov = get_at(d, lbit(i));
-                    ox = (int)((xb >> lbit(i)) & 1);
-                }
-            }
-            if constexpr (MW) {
-                if (own) { bc_s[rc & 1][0] = ov; bc_s[rc & 1][1] = ox; }
-            }
-            int v[1] = {tg};
-            const int ops[1] = {OP_MIN};
-            block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
-            if constexpr (MW) {
-                ov = bc_s[(rc - 1) & 1][0];
-                ox = bc_s[(rc - 1) & 1][1];
-            } else {
-                const int src = (i >> 3) & 31;
-                ov = __shfl_sync(FULL, ov, src);
-                ox = __shfl_sync(FULL, ox, src);
-            }
-            const int gmin = v[0];
-            if (E + gmin < ebest) set_best(best_key(tg, gmin), gmin);
-            do_flip(i, ov, ox);
-        }
-    };
-
-    // ---------------- batch control (R-12)
-    run_straight();
-    run_greedy();
-    int round = 0;
-    do {
-        phase_code = 2 + min(round, 100);
-        switch (algo) {
-        case ALG_MAXMIN: run_maxmin(); break;
-        case ALG_CYCLIC: run_cyclic(); break;
-        case ALG_RANDOM: run_random(); break;
-        case ALG_POSMIN: run_posmin(); break;
-        default: run_two(); break;
-        }
-        run_greedy();
-        round++;
-    } while (algo != ALG_TWO && flips < p.B);
+    }
 
     // ---------------- write back state and the result packet
     {
