@@ -175,6 +175,23 @@ __device__ __forceinline__ void neg_at(int32_t (&d)[EPT], int k)
     default: break;
     }
 }
+// sigma(x_k) of element k is byte k%4 of sg[k/4] (0x01 = +1, 0xFF = -1); flip it
+template <int NG>
+__device__ __forceinline__ void flip_sign_at(uint32_t (&sg)[NG], int k)
+{
+    const uint32_t m = 0xFEu << (8 * (k & 3));
+    switch (k >> 2) {
+#define DABS_G(j) \
+    case j:       \
+        if constexpr (j < NG) sg[j] ^= m; \
+        break;
+        DABS_G(0) DABS_G(1) DABS_G(2) DABS_G(3) DABS_G(4) DABS_G(5) DABS_G(6) DABS_G(7)
+        DABS_G(8) DABS_G(9) DABS_G(10) DABS_G(11) DABS_G(12) DABS_G(13) DABS_G(14) DABS_G(15)
+#undef DABS_G
+    default: break;
+    }
+}
+
 // first lane-of-chunk e in chunk c with mask bit set and d == m (or -1)
 template <int EPT, typename bits_t>
 __device__ __forceinline__ int first_in_chunk(const int32_t (&d)[EPT], bits_t M, int c, int m)
@@ -252,6 +269,16 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             d[8 * c + 0] = a.x; d[8 * c + 1] = a.y; d[8 * c + 2] = a.z; d[8 * c + 3] = a.w;
             d[8 * c + 4] = b.x; d[8 * c + 5] = b.y; d[8 * c + 6] = b.z; d[8 * c + 7] = b.w;
         }
+    }
+    // sigma(x_k) as signed bytes, 4 elements per word: the int8 operand of the
+    // IDP.2A dot products that apply Eq.(4) (one instruction per element)
+    uint32_t sg[EPT / 4];
+#pragma unroll
+    for (int g = 0; g < EPT / 4; g++) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) w |= (((xb >> (4 * g + j)) & 1) ? 0x01u : 0xFFu) << (8 * j);
+        sg[g] = w;
     }
     if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
     if (t == 0) {
@@ -686,13 +713,15 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
         }
         E += sv;
-        const bits_t negm = sx ? ~xb : xb;   // s_k = sigma(x_i) sigma(x_k) = -1 here
+        // sigma(x_i) = -1 (x_i = 0 before the flip): negate every sigma(x_k) byte
+        const uint32_t cmask = sx ? 0u : 0xFEFEFEFEu;
         if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
                 const int kk = lbit(si);
                 neg_at(d, kk);                   // Eq.(5)
                 xb ^= ONE << kk;
                 bdiff ^= ONE << kk;
+                flip_sign_at(sg, kk);            // (W_ii = 0: the update below leaves Delta_i alone)
             }
         }
         pos = (pos + TABU_RING - 1) & (TABU_RING - 1);
@@ -724,15 +753,19 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
 #pragma unroll
             for (int cc = 0; cc < CPP; cc++) {
                 const int c = qq * CPP + cc;
-                const uint32_t wv[4] = {rw[cc].x, rw[cc].y, rw[cc].z, rw[cc].w};
-#pragma unroll
-                for (int h = 0; h < 4; h++) {
-                    const int lo = (int)(int16_t)(wv[h] & 0xFFFFu);
-                    const int hi = (int)wv[h] >> 16;
-                    const int k0 = 8 * c + 2 * h, k1 = k0 + 1;
-                    d[k0] += ((negm >> k0) & 1) ? -lo : lo;   // Eq.(4)
-                    d[k1] += ((negm >> k1) & 1) ? -hi : hi;
-                }
+                // Eq.(4): Delta_k += W_ik sigma(x_i) sigma(x_k); the row word holds
+                // (W_i,k0, W_i,k1) as int16x2, B holds (s_k0, 0, 0, s_k1) as int8x4
+                const uint32_t g0 = sg[2 * c] ^ cmask, g1 = sg[2 * c + 1] ^ cmask;
+                const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
+                const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
+                d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);
+                d[8 * c + 1] = __dp2a_hi((int)rw[cc].x, (int)B0, d[8 * c + 1]);
+                d[8 * c + 2] = __dp2a_lo((int)rw[cc].y, (int)B1, d[8 * c + 2]);
+                d[8 * c + 3] = __dp2a_hi((int)rw[cc].y, (int)B1, d[8 * c + 3]);
+                d[8 * c + 4] = __dp2a_lo((int)rw[cc].z, (int)B2, d[8 * c + 4]);
+                d[8 * c + 5] = __dp2a_hi((int)rw[cc].z, (int)B2, d[8 * c + 5]);
+                d[8 * c + 6] = __dp2a_lo((int)rw[cc].w, (int)B3, d[8 * c + 6]);
+                d[8 * c + 7] = __dp2a_hi((int)rw[cc].w, (int)B3, d[8 * c + 7]);
             }
         }
         par_row ^= 1u;
