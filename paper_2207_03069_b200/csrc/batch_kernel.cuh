@@ -175,6 +175,40 @@ __device__ __forceinline__ void neg_at(int32_t (&d)[EPT], int k)
     default: break;
     }
 }
+// The owner of flipped element k: Delta_k <- -Delta_k (Eq.(5)) and sigma(x_k)
+// byte flipped, one jump table for both
+template <int EPT>
+__device__ __forceinline__ void owner_flip(int32_t (&d)[EPT], uint32_t (&sg)[EPT / 4], int k)
+{
+    const uint32_t m = 0xFEu << (8 * (k & 3));
+    switch (k) {
+#define DABS_CASE(j) \
+    case j:          \
+        if constexpr (j < EPT) { d[j] = -d[j]; sg[j >> 2] ^= m; } \
+        break;
+        DABS_CASE(0) DABS_CASE(1) DABS_CASE(2) DABS_CASE(3) DABS_CASE(4) DABS_CASE(5) DABS_CASE(6) DABS_CASE(7)
+        DABS_CASE(8) DABS_CASE(9) DABS_CASE(10) DABS_CASE(11) DABS_CASE(12) DABS_CASE(13) DABS_CASE(14) DABS_CASE(15)
+        DABS_CASE(16) DABS_CASE(17) DABS_CASE(18) DABS_CASE(19) DABS_CASE(20) DABS_CASE(21) DABS_CASE(22) DABS_CASE(23)
+        DABS_CASE(24) DABS_CASE(25) DABS_CASE(26) DABS_CASE(27) DABS_CASE(28) DABS_CASE(29) DABS_CASE(30) DABS_CASE(31)
+        DABS_CASE(32) DABS_CASE(33) DABS_CASE(34) DABS_CASE(35) DABS_CASE(36) DABS_CASE(37) DABS_CASE(38) DABS_CASE(39)
+        DABS_CASE(40) DABS_CASE(41) DABS_CASE(42) DABS_CASE(43) DABS_CASE(44) DABS_CASE(45) DABS_CASE(46) DABS_CASE(47)
+        DABS_CASE(48) DABS_CASE(49) DABS_CASE(50) DABS_CASE(51) DABS_CASE(52) DABS_CASE(53) DABS_CASE(54) DABS_CASE(55)
+        DABS_CASE(56) DABS_CASE(57) DABS_CASE(58) DABS_CASE(59) DABS_CASE(60) DABS_CASE(61) DABS_CASE(62) DABS_CASE(63)
+#undef DABS_CASE
+    default: break;
+    }
+}
+
+// min over all EPT values with 4 independent accumulators (ILP)
+template <int EPT>
+__device__ __forceinline__ int min_all(const int32_t (&d)[EPT])
+{
+    int a[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+#pragma unroll
+    for (int k = 0; k < EPT; k++) a[k & 3] = min(a[k & 3], d[k]);
+    return min(min(a[0], a[1]), min(a[2], a[3]));
+}
+
 // sigma(x_k) of element k is byte k%4 of sg[k/4] (0x01 = +1, 0xFF = -1); flip it
 template <int NG>
 __device__ __forceinline__ void flip_sign_at(uint32_t (&sg)[NG], int k)
@@ -245,6 +279,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
 
     extern __shared__ __align__(128) uint8_t dyn_smem[];
     const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // one W row, 2*n_pad bytes
+    uint8_t* tcnt = dyn_smem + 2 * p.n_pad;   // per element: occurrences in the last `tabu` flips
     __shared__ __align__(8) uint64_t mbar[NP];
     __shared__ int32_t ring_s[TABU_RING];
     __shared__ int32_t red_s[2][32][RED_W];
@@ -291,6 +326,10 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     const int algo = p.algo[s];
     const int tabu = p.tabu;
     const int T = p.T;
+    // tabu state (R-11): each thread counts its own elements' occurrences in
+    // the last `tabu` flips (shared memory) and keeps the bits count > 0 in tm
+#pragma unroll
+    for (int c = 0; c < C; c++) reinterpret_cast<uint2*>(tcnt)[(c << lgNT) + t] = make_uint2(0u, 0u);
     const uint32_t piece_bytes = (uint32_t)(2 * p.n_pad / NP);
     uint32_t par_row = 0;
     int flips = 0;
@@ -306,7 +345,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     // phases: 0 Straight, 1 Greedy, 2 main (R-12)
     int phase = 0, round = 0, tt = 0, cursor = 0;
     bool after_main = false;
-    bits_t tm = 0;                 // tabu mask of this thread's elements (main phases, R-11)
+    bits_t tm = 0;                 // tabu mask of this thread's elements (R-11)
+    for (int j = 0; j < tabu; j++) {
+        const int r = ring_s[j];
+        if (r >= 0 && owns(r)) { tcnt[r]++; tm |= ONE << lbit(r); }
+    }
 
     while (true) {
         // ---------------- phase transitions
@@ -329,15 +372,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             masked = false;                                        // Greedy
         } else {
             tt++;
-            if (tt == 1) {                                         // main run starts
-                cursor = 0;
-                tm = 0;
-                if (algo != ALG_TWO)
-                    for (int j = 0; j < tabu; j++) {
-                        const int r = ring_s[(pos + j) & (TABU_RING - 1)];
-                        if (r >= 0 && owns(r)) tm |= ONE << lbit(r);
-                    }
-            }
+            if (tt == 1) cursor = 0;                               // main run starts
             if (algo == ALG_CYCLIC) {                              // CyclicMin (R-7)
                 const int w = p.wtab[tt];
                 const int b0 = min(cursor + w, n), b1 = cursor + w - n;
@@ -401,8 +436,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 tsel = tg;
                 M1 = ALL;
             } else {
-#pragma unroll
-                for (int k = 0; k < EPT; k++) tg = min(tg, d[k]);
+                tg = min_all(d);
 #pragma unroll
                 for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
                 if (__any_sync(FULL, M1 != 0)) {      // warps without candidates skip
@@ -486,8 +520,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             sv = m;
         } else if (kind == 2) {
             // TwoNeighbor: scan, and the owner of fixed_i publishes Delta_i and x_i
-#pragma unroll
-            for (int kk = 0; kk < EPT; kk++) tg = min(tg, d[kk]);
+            tg = min_all(d);
             int ov = 0, ox = 0;
             const bool own = owns(fixed_i);
             if (__any_sync(FULL, own)) {
@@ -519,8 +552,12 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             int a1 = INT32_MAX, a2 = INT32_MIN;         // MaxMin: lo, hi; PositiveMin: pm, unused
             if (algo == ALG_MAXMIN) {
                 if (__all_sync(FULL, lane_plain)) {
+                    int m4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+                    int x4[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
 #pragma unroll
-                    for (int kk = 0; kk < EPT; kk++) { tg = min(tg, d[kk]); a2 = max(a2, d[kk]); }
+                    for (int kk = 0; kk < EPT; kk++) { m4[kk & 3] = min(m4[kk & 3], d[kk]); x4[kk & 3] = max(x4[kk & 3], d[kk]); }
+                    tg = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                    a2 = max(max(x4[0], x4[1]), max(x4[2], x4[3]));
                     a1 = tg;
                 } else {
 #pragma unroll
@@ -532,8 +569,15 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             } else {
                 unsigned tp = 0xFFFFFFFFu;   // min over eligible positive Delta as (Delta - 1), unsigned
                 if (__all_sync(FULL, (el | ~vb) == ALL)) {
+                    int m4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
+                    unsigned p4[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
 #pragma unroll
-                    for (int kk = 0; kk < EPT; kk++) { tg = min(tg, d[kk]); tp = min(tp, (unsigned)(d[kk] - 1)); }
+                    for (int kk = 0; kk < EPT; kk++) {
+                        m4[kk & 3] = min(m4[kk & 3], d[kk]);
+                        p4[kk & 3] = min(p4[kk & 3], (unsigned)(d[kk] - 1));
+                    }
+                    tg = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                    tp = min(min(p4[0], p4[1]), min(p4[2], p4[3]));
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < EPT; kk++) {
@@ -582,8 +626,12 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             for (int w = 0; w < CW; w++) pk[w] = 0;
             bits_t cb = 0;
 #pragma unroll
-            for (int kk = 0; kk < EPT; kk++)
-                if (d[kk] <= thr) cb |= ONE << kk;
+            for (int c = 0; c < C; c++) {
+                uint32_t byte = 0;
+#pragma unroll
+                for (int e = 0; e < 8; e++) byte |= (uint32_t)(d[8 * c + e] <= thr) << e;
+                cb |= (bits_t)byte << (8 * c);
+            }
             cb &= EL;
 #pragma unroll
             for (int c = 0; c < C; c++)
@@ -718,23 +766,18 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
                 const int kk = lbit(si);
-                neg_at(d, kk);                   // Eq.(5)
+                owner_flip(d, sg, kk);           // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
                 xb ^= ONE << kk;
                 bdiff ^= ONE << kk;
-                flip_sign_at(sg, kk);            // (W_ii = 0: the update below leaves Delta_i alone)
             }
         }
         pos = (pos + TABU_RING - 1) & (TABU_RING - 1);
         ring_s[pos] = si;
-        if (phase == 2 && tabu > 0 && algo != ALG_TWO) {
-            // tabu (R-11): si enters; the (tabu+1)-th most recent flip leaves
-            if (owns(si)) tm |= ONE << lbit(si);
+        if (tabu > 0) {
+            // tabu window (R-11): si enters, the (tabu+1)-th most recent flip leaves
+            if (owns(si)) { tcnt[si]++; tm |= ONE << lbit(si); }
             const int r = ring_s[(pos + tabu) & (TABU_RING - 1)];
-            if (r >= 0 && owns(r)) {
-                bool still = false;
-                for (int j = 0; j < tabu; j++) still |= ring_s[(pos + j) & (TABU_RING - 1)] == r;
-                if (!still) tm &= ~(ONE << lbit(r));
-            }
+            if (r >= 0 && owns(r) && --tcnt[r] == 0) tm &= ~(ONE << lbit(r));
         }
         if constexpr (TRACE) {
             if (t == 0 && s == p.trace_slot && flips < p.tr_cap) {

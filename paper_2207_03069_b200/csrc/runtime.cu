@@ -160,7 +160,7 @@ static BatchFn pick_batch(int C, bool mw, bool trace)
     }
 }
 
-static size_t row_smem(const dabs_ctx* c) { return (size_t)2 * c->n_pad; }   // one W row
+static size_t row_smem(const dabs_ctx* c) { return (size_t)3 * c->n_pad; }   // one W row + tabu counts
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
 {
