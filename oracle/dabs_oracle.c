@@ -314,11 +314,22 @@ static int sel_cyclicmin(search_t* s, int t, int* cursor, uint8_t* elig)
     return j;
 }
 
+/* lowbias32 (C. Wellons' hash prospector): a bijective 32-bit mixer */
+static uint32_t lowbias32(uint32_t x)
+{
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+uint32_t orc_lowbias32(uint32_t x) { return lowbias32(x); }
+
 /* RandomMin, integer form R-8:
    p16 = min(65536, max(floor(65536 t^3/T^3), floor(2^21/n)));
-   bit k is a candidate iff non-tabu and u16(k) < p16, u16(k) = 16-bit half
-   (k mod 8) of Philox(RANDMIN, k/8, slot, gen, step); argmin over candidates
-   (lowest index); empty -> argmin over eligible bits. */
+   bit k is a candidate iff non-tabu and u16(k) < p16, where u16(k) is the
+   16-bit half (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9) and
+   K = word 0 of Philox(RANDMIN, 0, slot, gen, step) -- one keyed counter per
+   flip, a cheap mixer per bit pair (the paper draws per-thread xorshift
+   numbers); argmin over candidates (lowest index); empty -> argmin
+   over eligible bits. */
 static int sel_randommin(search_t* s, int t, uint8_t* elig)
 {
     int n = s->n;
@@ -330,11 +341,11 @@ static int sel_randommin(search_t* s, int t, uint8_t* elig)
     if (p > 65536u) p = 65536u;
     int j = -1;
     uint32_t r[4];
+    rng4(s->seed, PUR_RANDMIN, 0, s->slot, s->gen, (uint32_t)s->flips, r);
+    const uint32_t K = r[0];
     for (int k = 0; k < n; k++) {
-        if (k % 8 == 0)   /* one Philox block serves bits 8c .. 8c+7 */
-            rng4(s->seed, PUR_RANDMIN, (uint32_t)(k / 8), s->slot, s->gen, (uint32_t)s->flips, r);
-        int h = k % 8;
-        uint32_t u16 = (r[h / 2] >> (16 * (h % 2))) & 0xFFFFu;
+        uint32_t h = lowbias32(K + (uint32_t)(k / 2) * 0x9E3779B9u);
+        uint32_t u16 = (h >> (16 * (k % 2))) & 0xFFFFu;
         if (!is_tabu(s, k) && u16 < p && (j < 0 || s->delta[k] < s->delta[j])) j = k;
     }
     if (j < 0) {

@@ -87,6 +87,8 @@ def lib():
         L.orc_world_get_packet.argtypes = [P, C.c_int, P, P, P, P, P, P]
         L.orc_world_get_stats.argtypes = [P, P, P]
         L.orc_world_get_best.argtypes = [P, P, P, P]
+        L.orc_lowbias32.argtypes = [u32]
+        L.orc_lowbias32.restype = u32
         L.orc_rank_pick.argtypes = [u32, u32]
         L.orc_rank_pick.restype = u32
         L.orc_build_target.argtypes = [C.c_int, P, P, P, C.c_int, u64, u32, u32, u32, u32, P]
@@ -122,6 +124,10 @@ def delta_closed(U: np.ndarray, x: np.ndarray) -> np.ndarray:
     d = np.zeros(U.shape[0], np.int32)
     lib().orc_delta_closed(_p(U), U.shape[0], _p(x), _p(d))
     return d
+
+
+def lowbias32(x: int) -> int:
+    return int(lib().orc_lowbias32(x))
 
 
 def rank_pick(u: int, m: int) -> int:

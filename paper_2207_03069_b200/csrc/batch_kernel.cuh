@@ -393,15 +393,19 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 const uint32_t p16 = (uint32_t)p.ptab[tt];
                 bits_t cand = vb;
                 if (p16 < 65536u) {
+                    // u16(k) = half (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9),
+                    // K = one Philox word per flip (R-8, R-16)
+                    const uint32_t K = rng4(p.seed, PUR_RANDMIN, 0, gslot, p.gen, (uint32_t)flips).x;
                     cand = 0;
-#pragma unroll 1
+#pragma unroll
                     for (int c = 0; c < C; c++) {
-                        const uint4 r = rng4(p.seed, PUR_RANDMIN, (uint32_t)((c << lgNT) + t), gslot, p.gen,
-                                             (uint32_t)flips);
-                        uint32_t byte = (uint32_t)((r.x & 0xFFFFu) < p16) | ((uint32_t)((r.x >> 16) < p16) << 1) |
-                                        ((uint32_t)((r.y & 0xFFFFu) < p16) << 2) | ((uint32_t)((r.y >> 16) < p16) << 3) |
-                                        ((uint32_t)((r.z & 0xFFFFu) < p16) << 4) | ((uint32_t)((r.z >> 16) < p16) << 5) |
-                                        ((uint32_t)((r.w & 0xFFFFu) < p16) << 6) | ((uint32_t)((r.w >> 16) < p16) << 7);
+                        const uint32_t j0 = (uint32_t)(((c << lgNT) + t) << 2);   // first pair of the chunk
+                        uint32_t byte = 0;
+#pragma unroll
+                        for (int h = 0; h < 4; h++) {
+                            const uint32_t x = lowbias32(K + (j0 + h) * 0x9E3779B9u);
+                            byte |= ((uint32_t)((x & 0xFFFFu) < p16) | ((uint32_t)((x >> 16) < p16) << 1)) << (2 * h);
+                        }
                         cand |= (bits_t)byte << (8 * c);
                     }
                 }

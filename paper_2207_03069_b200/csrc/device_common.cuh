@@ -36,6 +36,17 @@ __device__ __forceinline__ uint4 rng4(uint64_t seed, uint32_t purpose, uint32_t 
                    (uint32_t)(seed >> 32));
 }
 
+// lowbias32 mixer (R-8): bijective 32-bit hash, used per bit pair by RandomMin
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
 // floor(u * m / 2^32)  (R-15)
 __device__ __forceinline__ uint32_t pick_u(uint32_t u, uint32_t m)
 {

@@ -588,3 +588,25 @@ def test_tsp_small_reaches_pinned_optimum(orc):
     cfg = orc.Config(s_milli=100, b_milli=1000, pools=2, slots=8)
     E, X, _ = orc.System(U, cfg).run(seed=1, flip_budget=5 * 10**6, target=E_star)
     assert E == E_star
+
+
+def test_randommin_draws_uniform(orc):
+    """R-8: u16(k) = half (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9); the
+    candidate indicator u16 < p16 has probability p16/65536 (chi-square style
+    check over many keys), and the mixer is a bijection (no collisions)."""
+    rng = np.random.default_rng(17)
+    vals = []
+    for K in rng.integers(0, 2**32, size=40, dtype=np.uint64):
+        for j in range(500):
+            h = orc.lowbias32(int((int(K) + j * 0x9E3779B9) & 0xFFFFFFFF))
+            vals.append(h & 0xFFFF)
+            vals.append(h >> 16)
+    v = np.array(vals)
+    for p16 in (64, 2048, 32768, 60000):
+        f = (v < p16).mean()
+        p = p16 / 65536
+        assert abs(f - p) < 5 * np.sqrt(p * (1 - p) / v.size) + 1e-9
+    hist = np.bincount(v >> 12, minlength=16) / v.size
+    assert np.abs(hist - 1 / 16).max() < 0.01
+    xs = [orc.lowbias32(x) for x in range(0, 1 << 16)]
+    assert len(set(xs)) == len(xs)
