@@ -34,6 +34,7 @@ struct BatchParams {
     uint32_t gen;
     uint32_t slot_base;      // global id of local slot 0
     int slot0;               // first local slot of this launch (blockIdx.x offset)
+    const int32_t* order;    // optional launch order of the slots (longest batches first)
     uint32_t* X;             // [slots][nwp]   persistent x (R-14)
     int32_t* delta;          // [slots][n_pad] persistent Delta (pads = INT32_MAX)
     int64_t* E;              // [slots]
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     const int NT = MW ? (int)blockDim.x : 32;
     const int lgNT = MW ? 31 - __clz(NT) : 5;
     const int lane = t & 31, wid = t >> 5, NW = NT >> 5;
-    const int s = p.slot0 + (int)blockIdx.x;
+    const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
     const int n = p.n;
 
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     __shared__ int32_t ring_s[TABU_RING];
     __shared__ int32_t red_s[2][32][RED_W];
     __shared__ int32_t bc_s[2][4];
+    __shared__ int32_t sel_s[4];   // MaxMin/PositiveMin pick, published through the row mbarrier
 
     // ---------------- load the slot's persistent state (R-14)
     int32_t d[EPT];
@@ -628,18 +630,24 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             uint32_t pk[CW];
 #pragma unroll
             for (int w = 0; w < CW; w++) pk[w] = 0;
-            bits_t cb = 0;
+            if (__all_sync(FULL, EL == ALL)) {
 #pragma unroll
-            for (int c = 0; c < C; c++) {
-                uint32_t byte = 0;
+                for (int c = 0; c < C; c++) {
+                    uint32_t cnt = 0;
 #pragma unroll
-                for (int e = 0; e < 8; e++) byte |= (uint32_t)(d[8 * c + e] <= thr) << e;
-                cb |= (bits_t)byte << (8 * c);
+                    for (int e = 0; e < 8; e++) cnt += (uint32_t)(d[8 * c + e] <= thr);
+                    pk[c >> 1] += cnt << (16 * (c & 1));
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    uint32_t byte = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) byte |= (uint32_t)(d[8 * c + e] <= thr) << e;
+                    byte &= (uint32_t)(EL >> (8 * c)) & 0xFFu;
+                    pk[c >> 1] += (uint32_t)__popc(byte) << (16 * (c & 1));
+                }
             }
-            cb &= EL;
-#pragma unroll
-            for (int c = 0; c < C; c++)
-                pk[c >> 1] += (uint32_t)__popc((uint32_t)((cb >> (8 * c)) & 0xFFu)) << (16 * (c & 1));
             uint32_t wt[CW];
 #pragma unroll
             for (int w = 0; w < CW; w++) wt[w] = warp_add(pk[w]);
@@ -689,7 +697,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 uint32_t mybyte = 0;
 #pragma unroll
                 for (int c = 0; c < C; c++)
-                    if (c == cs) mybyte = (uint32_t)((cb >> (8 * c)) & 0xFFu);
+                    if (c == cs) {
+#pragma unroll
+                        for (int e = 0; e < 8; e++) mybyte |= (uint32_t)(d[8 * c + e] <= thr) << e;
+                        mybyte &= (uint32_t)(EL >> (8 * c)) & 0xFFu;
+                    }
                 const int x = __popc(mybyte);
                 int y = x;
 #pragma unroll
@@ -708,11 +720,17 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 }
             }
             if constexpr (MW) {
-                const int par2 = rc & 1;
-                rc++;
-                if (gi >= 0) { bc_s[par2][0] = gi; bc_s[par2][1] = lv; bc_s[par2][2] = lx; }
-                __syncthreads();
-                si = bc_s[par2][0]; sv = bc_s[par2][1]; sx = bc_s[par2][2];
+                // the locating thread publishes the pick and starts the row copy
+                // itself; everybody else learns (i, Delta_i, x_i) from the row's
+                // mbarrier (arrive = release, try_wait = acquire): no CTA barrier
+                if (gi >= 0) {
+                    sel_s[0] = gi; sel_s[1] = lv; sel_s[2] = lx;
+                    fence_proxy_async();
+                    const char* src = reinterpret_cast<const char*>(p.W) + (size_t)gi * (size_t)(2 * p.n_pad);
+#pragma unroll
+                    for (int qq = 0; qq < NP; qq++)
+                        bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
+                }
             } else {
                 const int src = __ffs(__ballot_sync(FULL, gi >= 0)) - 1;
                 si = __shfl_sync(FULL, gi, src);
@@ -757,7 +775,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
 
         // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
         // every thread has passed the last exchange: the row buffer is free
-        if (t == 0) {
+        const bool pre_issued = MW && kind == 1;
+        if (pre_issued) {
+            mbar_wait(&mbar[0], par_row);
+            si = sel_s[0]; sv = sel_s[1]; sx = sel_s[2];
+        } else if (t == 0) {
             fence_proxy_async();
             const char* src = reinterpret_cast<const char*>(p.W) + (size_t)si * (size_t)(2 * p.n_pad);
 #pragma unroll

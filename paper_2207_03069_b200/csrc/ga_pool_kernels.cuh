@@ -189,6 +189,38 @@ __global__ void ga_seed_kernel(GaConst g, const PoolView* __restrict__ pools, ui
     }
 }
 
+// Launch order for the batch kernel: slots whose batches cost the most start
+// first (longest-processing-time order; the results do not depend on it).
+// Cost classes from measured per-algorithm flip rates: TwoNeighbor (2n-1 main
+// flips), MaxMin, PositiveMin, RandomMin, CyclicMin.  One CTA, stable.
+__global__ void order_kernel(const uint8_t* __restrict__ palgo, int nslots, int32_t* __restrict__ order)
+{
+    __shared__ int cnt[5];
+    __shared__ int base[5];
+    const int cls_of[5] = {1, 4, 3, 2, 0};   // by algorithm id: MaxMin, CyclicMin, RandomMin, PositiveMin, Two
+    if (threadIdx.x < 5) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) atomicAdd(&cnt[cls_of[palgo[s]]], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int c = 0; c < 5; c++) { base[c] = a; a += cnt[c]; }
+    }
+    __syncthreads();
+    // stable scatter: one warp per class walks the slots in order
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < 5) {
+        int pos = base[w];
+        for (int s0 = 0; s0 < nslots; s0 += 32) {
+            const int s = s0 + lane;
+            const bool m = s < nslots && cls_of[palgo[s]] == w;
+            const unsigned bal = __ballot_sync(0xffffffffu, m);
+            if (m) order[pos + __popc(bal & ((1u << lane) - 1u))] = s;
+            pos += __popc(bal);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ a8 pool merge
 // One CTA (1024 threads) per local pool (R-18).  The new pool
 // is the first cap entries of the (E, seq)-sorted old ++ new list with

@@ -63,6 +63,7 @@ struct dabs_ctx {
     uint8_t *palgo = nullptr, *pgenop = nullptr;
     uint32_t* best = nullptr;
     int64_t *ebest = nullptr, *flips = nullptr;
+    int32_t* order = nullptr;             // batch launch order (longest first)
     PoolView* pools_d = nullptr;          // [P+1]
     std::vector<PoolView> pools_h;        // host copy of the views
     MergeArgs margs{};
@@ -348,7 +349,7 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
 #define AB(ptr, count) if ((st = dalloc(c, &(ptr), (count))) != DABS_OK) return bail(st)
     AB(c->X, ns * nwp); AB(c->delta, ns * c->n_pad); AB(c->E, ns); AB(c->ring, ns * TABU_RING);
     AB(c->D, ns * nwp); AB(c->palgo, ns); AB(c->pgenop, ns);
-    AB(c->best, ns * nwp); AB(c->ebest, ns); AB(c->flips, ns);
+    AB(c->best, ns * nwp); AB(c->ebest, ns); AB(c->flips, ns); AB(c->order, ns);
     AB(c->dispatch, P * N_ALG * N_GEN); AB(c->inserted, P * N_ALG * N_GEN);
     AB(c->flip_total, 1); AB(c->xbytes, (size_t)n);
     c->pools_h.resize(P + 1);
@@ -431,9 +432,11 @@ extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)
     return DABS_OK;
 }
 
-static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0, int count, bool trace)
+static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0, int count, bool trace,
+                                const int32_t* order = nullptr)
 {
     BatchParams p = batch_params(c, seed, gen, slot0);
+    p.order = order;
     BatchFn fn = pick_batch(c->C, c->mw, trace);
     fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
     CK(cudaGetLastError());
@@ -455,7 +458,9 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], st));
     // a4-a7: one batch search per slot (the hot loop)
-    dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0);
+    order_kernel<<<1, 256, 0, st>>>(c->palgo, c->slots, c->order);
+    CK(cudaGetLastError());
+    dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0, c->order);
     if (s1 != DABS_OK) return s1;
     CK(cudaEventRecord(c->ev[2], st));
     // a8: pool merge
