@@ -259,14 +259,18 @@ def main():
     avg_batch_ms = float(np.mean(batch_ms))
     bytes_per_launch = float(np.mean(local_flips)) * 2 * n
     achieved = bytes_per_launch / (avg_batch_ms / 1e3) / 1e9
-    traffic = None
+    # DRAM traffic of the same kernel from the committed ncu --set full capture
+    # (profiles/r01_ncu_batch_<workload>.json), scaled to this run's launch
+    traffic, traffic_src = None, None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get(args.workload, {}).get("dram_bytes_per_launch")
+        prof = json.load(open(os.path.join(ROOT, "profiles", f"r01_ncu_batch_{args.workload.lower()}.json")))
+        traffic = prof["dram_bytes_per_flip"] * float(np.mean(local_flips))
+        traffic_src = (f"ncu --set full capture {os.path.basename(prof['report'])}: "
+                       f"{prof['dram_bytes_per_flip']:.0f} DRAM bytes per flip x flips per launch")
     except Exception:  # noqa: BLE001
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": "batch_kernel",
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": "batch_kernel",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
                 "bytes_per_flip": 2 * n, "batch_share_of_step": sum(batch_ms) / t_ms if world == 1 else None}
 
@@ -277,6 +281,7 @@ def main():
         "config": config_of(args.workload, U, meta, solver), "roofline": roofline,
         "gpu_launches": 5 * args.steps, "clocks": clk,
         "per_gpu_flips_per_s": value / world,
+        "flips_per_step": [int(x) for x in local_flips], "batch_ms_per_step": [float(x) for x in batch_ms],
         "best_energy": st1.best_energy, "generations": int(st1.generations),
     }
     # ---- e2e: through the public API from pinned host memory, every step:
