@@ -28,6 +28,7 @@ struct BatchParams {
     const int16_t* W;        // [n][n_pad] symmetric, zero diagonal, zero padding
     const int32_t* wtab;     // [T+1] CyclicMin width w(t)       (R-7)
     const int32_t* ptab;     // [T+1] RandomMin threshold p16(t) (R-8)
+    const int32_t* rmax;     // [n] max_k |W_ik|: bounds how far any Delta can fall per flip
     int n, n_pad, nwp;       // nwp = n_pad / 32 words per bit vector
     int T, B, tabu;
     uint64_t seed;
@@ -348,6 +349,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     int phase = 0, round = 0, tt = 0, cursor = 0;
     bool after_main = false;
     bits_t tm = 0;                 // tabu mask of this thread's elements (R-11)
+    // Lower bound on min_k Delta_k.  Step 1 can only improve BEST if
+    // E + min Delta < E(BEST); while E + glb >= E(BEST) the exact global
+    // minimum is not needed (the paper's "BEST updates are rare").
+    // After flipping i: Delta_k moves by at most |W_ik|, Delta_i becomes -Delta_i.
+    int64_t glb = INT64_MIN / 4;
     for (int j = 0; j < tabu; j++) {
         const int r = ring_s[j];
         if (r >= 0 && owns(r)) { tcnt[r]++; tm |= ONE << lbit(r); }
@@ -381,11 +387,15 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 bits_t wm = 0;
 #pragma unroll
                 for (int c = 0; c < C; c++) {
-                    const int base = gidx(c, 0);
-                    const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
-                    if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
-                    const int hi2 = min(b1 - base, 8);
-                    if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
+                    // uniform: does the window meet chunk c at all (its span is NT*8 elements)?
+                    const int s0 = (c << lgNT) << 3, s1 = s0 + (NT << 3);
+                    if ((cursor < s1 && b0 > s0) || b1 > s0) {
+                        const int base = gidx(c, 0);
+                        const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
+                        if (lo < hi) wm |= (bits_t)((((1u << (hi - lo)) - 1u) << lo)) << (8 * c);
+                        const int hi2 = min(b1 - base, 8);
+                        if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
+                    }
                 }
                 cursor = (cursor + w) % n;
                 M1 = wm & ~tm;
@@ -424,6 +434,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
 
         // ---------------- Step 1 + Step 2: scans and one exchange
+        const bool skip_g = E + glb >= ebest;   // no 1-bit neighbour can beat BEST (uniform)
         int si = 0, sv = 0, sx = 0;     // selected bit, its Delta, its x (uniform)
         int gmin = 0, tg = INT32_MAX;
         int key = INT32_MAX;            // argmin key of the rule (kind 0)
@@ -442,7 +453,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 tsel = tg;
                 M1 = ALL;
             } else {
-                tg = min_all(d);
+                if (!skip_g) tg = min_all(d);
 #pragma unroll
                 for (int c = 0; c < C; c++) gm[c] = INT32_MAX;
                 if (__any_sync(FULL, M1 != 0)) {      // warps without candidates skip
@@ -504,7 +515,15 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 const int ops1[1] = {OP_MIN};
                 block_reduce<MW>(v2, ops1, red_s, rc, lane, wid, NW);
                 bits_t MM = M2;
-                if (v2[0] == INT32_MAX) { MM = vb; t2 = tg; v2[0] = gmin; }
+                if (v2[0] == INT32_MAX) {
+                    if (skip_g) {                   // exact global minimum needed after all
+                        tg = min_all(d);
+                        int v3[1] = {tg};
+                        block_reduce<MW>(v3, ops1, red_s, rc, lane, wid, NW);
+                        gmin = v3[0];
+                    }
+                    MM = vb; t2 = tg; v2[0] = gmin;
+                }
                 m = v2[0];
                 int k2 = INT32_MAX;
                 if (__any_sync(FULL, t2 == m))
@@ -526,7 +545,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             sv = m;
         } else if (kind == 2) {
             // TwoNeighbor: scan, and the owner of fixed_i publishes Delta_i and x_i
-            tg = min_all(d);
+            if (!skip_g) tg = min_all(d);
             int ov = 0, ox = 0;
             const bool own = owns(fixed_i);
             if (__any_sync(FULL, own)) {
@@ -575,15 +594,11 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             } else {
                 unsigned tp = 0xFFFFFFFFu;   // min over eligible positive Delta as (Delta - 1), unsigned
                 if (__all_sync(FULL, (el | ~vb) == ALL)) {
-                    int m4[4] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX};
                     unsigned p4[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
 #pragma unroll
-                    for (int kk = 0; kk < EPT; kk++) {
-                        m4[kk & 3] = min(m4[kk & 3], d[kk]);
-                        p4[kk & 3] = min(p4[kk & 3], (unsigned)(d[kk] - 1));
-                    }
-                    tg = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+                    for (int kk = 0; kk < EPT; kk++) p4[kk & 3] = min(p4[kk & 3], (unsigned)(d[kk] - 1));
                     tp = min(min(p4[0], p4[1]), min(p4[2], p4[3]));
+                    if (!skip_g) tg = min_all(d);
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < EPT; kk++) {
@@ -740,6 +755,9 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
 
         // ---------------- Step 1: BEST (R-2, R-3)
+        const bool g_exact = !skip_g || phase == 1 || (kind == 1 && algo == ALG_MAXMIN);
+        if (g_exact) glb = gmin;
+        else gmin = INT32_MAX;                  // not computed: cannot improve BEST
         if (E + gmin < ebest) {
             int bk = key;
             if (kind != 0 || masked) {
@@ -787,6 +805,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
         }
         E += sv;
+        glb = min(glb - (int64_t)p.rmax[si], (int64_t)-sv);
         // sigma(x_i) = -1 (x_i = 0 before the flip): negate every sigma(x_k) byte
         const uint32_t cmask = sx ? 0u : 0xFEFEFEFEu;
         if (__any_sync(FULL, owns(si))) {

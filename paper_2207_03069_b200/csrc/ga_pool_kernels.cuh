@@ -66,6 +66,24 @@ __global__ void symmetrize_kernel(const int16_t* __restrict__ U, int n, int n_pa
     }
 }
 
+// rmax[i] = max_{k != i} |W_ik| (one CTA per row): how far any Delta_k can
+// move in one flip of bit i (batch kernel's lower bound on min Delta)
+__global__ void rowmax_kernel(const int16_t* __restrict__ W, int n, int n_pad, int32_t* __restrict__ rmax)
+{
+    const int i = blockIdx.x;
+    int m = 0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) m = max(m, abs((int)W[(size_t)i * n_pad + k]));
+    m = __reduce_max_sync(0xffffffffu, m);
+    __shared__ int red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t = max(t, red[w]);
+        rmax[i] = t;
+    }
+}
+
 // ------------------------------------------------------------------ a2 init
 // Slots: X = 0, E = 0, Delta = diag (pads INT32_MAX), empty tabu ring (R-14).
 __global__ void init_slots_kernel(int slots, int n_pad, int nwp, const int32_t* __restrict__ diag,

@@ -54,6 +54,7 @@ struct dabs_ctx {
     std::vector<void*> allocs;
     int16_t* W = nullptr;
     int32_t* diag = nullptr;
+    int32_t* rmax = nullptr;
     int32_t *wtab = nullptr, *ptab = nullptr;
     uint32_t* X = nullptr;
     int32_t* delta = nullptr;
@@ -166,7 +167,7 @@ static size_t row_smem(const dabs_ctx* c) { return (size_t)3 * c->n_pad; }   // 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
 {
     BatchParams p{};
-    p.W = c->W; p.wtab = c->wtab; p.ptab = c->ptab;
+    p.W = c->W; p.wtab = c->wtab; p.ptab = c->ptab; p.rmax = c->rmax;
     p.n = c->n; p.n_pad = c->n_pad; p.nwp = c->nwp;
     p.T = c->T; p.B = c->B; p.tabu = c->tabu;
     p.seed = seed; p.gen = gen;
@@ -310,6 +311,8 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
         dim3 grid((c->n_pad + 31) / 32, (n + 31) / 32), blk(32, 8);
         symmetrize_kernel<<<grid, blk, 0, c->stream>>>(U, n, c->n_pad, c->W, c->diag);
     }
+    if ((st = dalloc(c, &c->rmax, n)) != DABS_OK) return bail(st);
+    rowmax_kernel<<<n, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->rmax);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess)
         return bail(fail(DABS_E_CUDA, "symmetrize: %s", cudaGetErrorString(cudaGetLastError())));
     // free the staging copy
