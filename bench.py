@@ -40,9 +40,11 @@ def parse():
     ap.add_argument("--impl", default="dabs", choices=["dabs", "reference"])
     ap.add_argument("--workload", default="R32K", choices=["K16", "GS800", "TSP32", "K2000s", "R32K"])
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--slots", type=int, default=0, help="slots per pool (0 = library default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample size (cpu_baseline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tts", action="store_true")
     return ap.parse_args()
 
 
@@ -206,7 +208,8 @@ def main():
     n = U.shape[0]
     stream = torch.cuda.Stream()
     solver = Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=meta.get("pools", 1),
-                    slots=meta.get("slots", 0), rank=rank, world=world, device=torch.cuda.current_device(),
+                    slots=args.slots or meta.get("slots", 0), rank=rank, world=world,
+                    device=torch.cuda.current_device(),
                     stream=stream.cuda_stream, exchange=torch_exchange() if world > 1 else None)
     solver.reset(args.seed)
     for _ in range(args.warmup):
@@ -298,7 +301,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             s2 = Solver(Wnp, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=meta.get("pools", 1),
-                        slots=meta.get("slots", 0), rank=rank, world=world,
+                        slots=args.slots or meta.get("slots", 0), rank=rank, world=world,
                         device=torch.cuda.current_device(), stream=stream.cuda_stream,
                         exchange=torch_exchange() if world > 1 else None)
             E, x = s2.run(seed=args.seed + k, flip_budget=budget)
@@ -313,6 +316,24 @@ def main():
         out["e2e"] = {"value": e2e_flips / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(2 * n * n),
                       "d2h_bytes_per_step": int(n + 8), "steps": max(1, min(args.steps, 3)),
                       "what": "dabs_create(W from pinned host) + dabs_run(one generation) + best readback"}
+    # ---- time-to-target on the workload with a pinned optimum (TSP32 cycle
+    # metric, E* = -19872, R-22): success rate and mean TTS over successes
+    # (the paper's protocol), every rank participating (SPMD)
+    if not args.no_tts:
+        Ut, mt = wl.make("TSP32", seed=1)
+        st_ = Solver(Ut, s_milli=mt["s_milli"], b_milli=mt["b_milli"], pools=8, rank=rank, world=world,
+                     device=torch.cuda.current_device(), stream=stream.cuda_stream, target=mt["target"],
+                     time_limit_ns=int(20e9), exchange=torch_exchange() if world > 1 else None)
+        tts = []
+        for r in range(3):
+            E, _ = st_.run(seed=1000 + r, flip_budget=1 << 62)
+            tts.append((E <= mt["target"], st_.stats().time_to_best_ns / 1e9))
+        st_.close()
+        ok = [x for o, x in tts if o]
+        out["time_to_target"] = {"workload": "TSP32", "target": int(mt["target"]), "runs": len(tts),
+                                 "success_rate": len(ok) / len(tts),
+                                 "mean_tts_s": float(np.mean(ok)) if ok else None, "limit_s": 20,
+                                 "timer": "host wall clock from dabs_reset to the generation that found it"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         f, dt, cores, quota = oracle_sample(U, meta, args.cpu_seconds, args.seed)
         out["cpu_baseline"] = {"value": f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",

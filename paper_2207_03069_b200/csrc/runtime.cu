@@ -274,7 +274,9 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->mw, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = prop.multiProcessorCount * occ;
-        c->S = (2 * conc + c->P - 1) / c->P;   // about two waves per generation
+        c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
+                                                // (TwoNeighbor runs 2n-1 main flips), more
+                                                // waves let the block scheduler balance them
     }
     c->slots = c->P * c->S;
     if ((int64_t)c->slots * (cfg.world) >= (1ll << 31)) return bail(fail(DABS_E_ARG, "too many slots"));
