@@ -29,6 +29,7 @@ struct BatchParams {
     const int32_t* wtab;     // [T+1] CyclicMin width w(t)       (R-7)
     const int32_t* ptab;     // [T+1] RandomMin threshold p16(t) (R-8)
     const int32_t* rmax;     // [n] max_k |W_ik|: bounds how far any Delta can fall per flip
+    double invT3;            // 1 / T^3 (MaxMin span estimate, corrected exactly)
     int n, n_pad, nwp;       // nwp = n_pad / 32 words per bit vector
     int T, B, tabu;
     uint64_t seed;
@@ -250,11 +251,11 @@ __device__ __forceinline__ int first_in_chunk(const int32_t (&d)[EPT], bits_t M,
 }
 
 // floor(a * f / q) exactly, a < 2^33, f, q <= 2^48 (MaxMin span, R-6):
-// a double estimate corrected with 128-bit integer products.
-__device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_t q)
+// a double estimate (inv_q = 1/q precomputed) corrected with 128-bit integer products.
+__device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_t q, double inv_q)
 {
     const unsigned __int128 num = (unsigned __int128)a * f;
-    uint64_t est = (uint64_t)((double)a * (double)f / (double)q);
+    uint64_t est = (uint64_t)((double)a * (double)f * inv_q);
     while ((unsigned __int128)est * q > num) est--;
     while ((unsigned __int128)(est + 1) * q <= num) est++;
     return est;
@@ -309,14 +310,18 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         }
     }
     // sigma(x_k) as signed bytes, 4 elements per word: the int8 operand of the
-    // IDP.2A dot products that apply Eq.(4) (one instruction per element)
-    uint32_t sg[EPT / 4];
+    // IDP.2A dot products that apply Eq.(4) (one instruction per element).
+    // Registers for one warp per search; shared memory ([EPT/16][NT] uint4,
+    // conflict-free) for the CTA tier, where registers are the limit.
+    uint32_t sg[MW ? 1 : EPT / 4];
+    uint4* sgs = reinterpret_cast<uint4*>(dyn_smem + 3 * p.n_pad);
 #pragma unroll
     for (int g = 0; g < EPT / 4; g++) {
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < 4; j++) w |= (((xb >> (4 * g + j)) & 1) ? 0x01u : 0xFFu) << (8 * j);
-        sg[g] = w;
+        if constexpr (MW) reinterpret_cast<uint32_t*>(sgs)[(((g >> 2) << lgNT) + t) * 4 + (g & 3)] = w;
+        else sg[g] = w;
     }
     if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
     if (t == 0) {
@@ -354,6 +359,31 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     // minimum is not needed (the paper's "BEST updates are rare").
     // After flipping i: Delta_k moves by at most |W_ik|, Delta_i becomes -Delta_i.
     int64_t glb = INT64_MIN / 4;
+
+    // RandomMin candidates of main step ttv at batch flip fl (R-8): u16(k) = half
+    // (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9), K = one Philox word per flip
+    auto rand_cand = [&](int ttv, int fl) -> bits_t {
+        const uint32_t p16 = (uint32_t)p.ptab[ttv];
+        if (p16 >= 65536u) return vb;
+        const uint32_t K = rng4(p.seed, PUR_RANDMIN, 0, gslot, p.gen, (uint32_t)fl).x;
+        bits_t cand = 0;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            const uint32_t j0 = (uint32_t)(((c << lgNT) + t) << 2);   // first pair of the chunk
+            uint32_t byte = 0;
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                const uint32_t x = lowbias32(K + (j0 + h) * 0x9E3779B9u);
+                byte |= ((uint32_t)((x & 0xFFFFu) < p16) | ((uint32_t)((x >> 16) < p16) << 1)) << (2 * h);
+            }
+            cand |= (bits_t)byte << (8 * c);
+        }
+        return cand;
+    };
+    // (MW) the next main step's draws, computed while the row is in flight
+    int pre_for = -1;
+    bits_t cand_pre = 0;
+    uint4 r_pre = make_uint4(0, 0, 0, 0);
     for (int j = 0; j < tabu; j++) {
         const int r = ring_s[j];
         if (r >= 0 && owns(r)) { tcnt[r]++; tm |= ONE << lbit(r); }
@@ -402,25 +432,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 M2 = wm;
                 fb = 1;
             } else if (algo == ALG_RANDOM) {                       // RandomMin (R-8)
-                const uint32_t p16 = (uint32_t)p.ptab[tt];
-                bits_t cand = vb;
-                if (p16 < 65536u) {
-                    // u16(k) = half (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9),
-                    // K = one Philox word per flip (R-8, R-16)
-                    const uint32_t K = rng4(p.seed, PUR_RANDMIN, 0, gslot, p.gen, (uint32_t)flips).x;
-                    cand = 0;
-#pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        const uint32_t j0 = (uint32_t)(((c << lgNT) + t) << 2);   // first pair of the chunk
-                        uint32_t byte = 0;
-#pragma unroll
-                        for (int h = 0; h < 4; h++) {
-                            const uint32_t x = lowbias32(K + (j0 + h) * 0x9E3779B9u);
-                            byte |= ((uint32_t)((x & 0xFFFFu) < p16) | ((uint32_t)((x >> 16) < p16) << 1)) << (2 * h);
-                        }
-                        cand |= (bits_t)byte << (8 * c);
-                    }
-                }
+                const bits_t cand = (MW && pre_for == flips) ? cand_pre : rand_cand(tt, flips);
                 M1 = cand & ~tm & vb;
                 M2 = ~tm & vb;
                 fb = 2;
@@ -614,8 +626,10 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             gmin = v[0];
             bits_t EL = el;
             int thr;
-            const uint4 r = rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
-                                 (uint32_t)flips);
+            const uint4 r = (MW && pre_for == flips)
+                                ? r_pre
+                                : rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
+                                       (uint32_t)flips);
             if (!v[3]) {
                 // every bit tabu: drop tabu (R-11)
                 EL = vb;
@@ -634,7 +648,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             if (algo == ALG_MAXMIN) {
                 const uint64_t uu = (uint64_t)(T - tt);
                 const uint64_t span = muldiv_floor((uint64_t)((int64_t)v[2] - v[1]), uu * uu * uu,
-                                                   (uint64_t)T * T * T);
+                                                   (uint64_t)T * T * T, p.invT3);
                 thr = (int)((int64_t)v[1] + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32));
                 u = r.y;
             } else {
@@ -811,7 +825,13 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
         if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
                 const int kk = lbit(si);
-                owner_flip(d, sg, kk);           // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
+                if constexpr (MW) {
+                    neg_at(d, kk);               // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
+                    const int g = kk >> 2;
+                    reinterpret_cast<uint8_t*>(sgs)[((((g >> 2) << lgNT) + t) * 4 + (g & 3)) * 4 + (kk & 3)] ^= 0xFEu;
+                } else {
+                    owner_flip(d, sg, kk);       // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
+                }
                 xb ^= ONE << kk;
                 bdiff ^= ONE << kk;
             }
@@ -832,18 +852,39 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             }
         }
         flips++;
+        if constexpr (MW) {
+            if (phase == 2 && tt < T && algo != ALG_CYCLIC && algo != ALG_TWO) {
+                if (algo == ALG_RANDOM) cand_pre = rand_cand(tt + 1, flips);
+                else r_pre = rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
+                                  (uint32_t)flips);
+                pre_for = flips;
+            }
+        }
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) {
             mbar_wait(&mbar[qq], par_row);
             uint4 rw[CPP];
 #pragma unroll
             for (int cc = 0; cc < CPP; cc++) rw[cc] = row_s[((qq * CPP + cc) << lgNT) + t];
+            uint4 sw[(CPP + 1) / 2];
+            if constexpr (MW) {
+#pragma unroll
+                for (int j = 0; j < (CPP + 1) / 2; j++) sw[j] = sgs[(((qq * CPP) / 2 + j) << lgNT) + t];
+            }
 #pragma unroll
             for (int cc = 0; cc < CPP; cc++) {
                 const int c = qq * CPP + cc;
                 // Eq.(4): Delta_k += W_ik sigma(x_i) sigma(x_k); the row word holds
                 // (W_i,k0, W_i,k1) as int16x2, B holds (s_k0, 0, 0, s_k1) as int8x4
-                const uint32_t g0 = sg[2 * c] ^ cmask, g1 = sg[2 * c + 1] ^ cmask;
+                uint32_t g0, g1;
+                if constexpr (MW) {
+                    const uint4 q4 = sw[cc >> 1];
+                    g0 = ((c & 1) ? q4.z : q4.x) ^ cmask;
+                    g1 = ((c & 1) ? q4.w : q4.y) ^ cmask;
+                } else {
+                    g0 = sg[2 * c] ^ cmask;
+                    g1 = sg[2 * c + 1] ^ cmask;
+                }
                 const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
                 const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
                 d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);

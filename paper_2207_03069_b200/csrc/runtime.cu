@@ -162,12 +162,16 @@ static BatchFn pick_batch(int C, bool mw, bool trace)
     }
 }
 
-static size_t row_smem(const dabs_ctx* c) { return (size_t)3 * c->n_pad; }   // one W row + tabu counts
+static size_t row_smem(const dabs_ctx* c)   // one W row + tabu counts (+ sigma bytes, CTA tier)
+{
+    return (size_t)(c->mw ? 4 : 3) * c->n_pad;
+}
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
 {
     BatchParams p{};
     p.W = c->W; p.wtab = c->wtab; p.ptab = c->ptab; p.rmax = c->rmax;
+    p.invT3 = 1.0 / ((double)c->T * (double)c->T * (double)c->T);
     p.n = c->n; p.n_pad = c->n_pad; p.nwp = c->nwp;
     p.T = c->T; p.B = c->B; p.tabu = c->tabu;
     p.seed = seed; p.gen = gen;
