@@ -250,14 +250,16 @@ __device__ __forceinline__ int first_in_chunk(const int32_t (&d)[EPT], bits_t M,
     return r;
 }
 
-// floor(a * f / q) exactly, a < 2^33, f, q <= 2^48 (MaxMin span, R-6):
-// a double estimate (inv_q = 1/q precomputed) corrected with 128-bit integer products.
+// floor(a * f / q) exactly, a < 2^32, f, q <= 2^48 (MaxMin span, R-6): a double
+// estimate (inv_q = 1/q precomputed; relative error ~2^-50, so the estimate is
+// off by at most one) corrected once with the remainder a*f - est*q, whose
+// true value is tiny, computed exactly in wrapping 64-bit arithmetic.
 __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_t q, double inv_q)
 {
-    const unsigned __int128 num = (unsigned __int128)a * f;
     uint64_t est = (uint64_t)((double)a * (double)f * inv_q);
-    while ((unsigned __int128)est * q > num) est--;
-    while ((unsigned __int128)(est + 1) * q <= num) est++;
+    const int64_t rem = (int64_t)(a * f - est * q);
+    if (rem < 0) est--;
+    else if ((uint64_t)rem >= q) est++;
     return est;
 }
 
