@@ -94,6 +94,16 @@ void dabs_config_default(dabs_config* cfg);
  * and pools.  *out receives the context (NULL on failure). */
 dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg, dabs_ctx** out);
 
+/* Same, from a sparse upper triangle in CSR form (host arrays, caller-owned,
+ * copied): row i's off-diagonal coefficients W_ij, j > i, are
+ * val[row_ptr[i] .. row_ptr[i+1]) at columns col[...] (strictly increasing,
+ * each > i; zero values allowed), diag[i] = W_ii.  A column <= its row ->
+ * DABS_E_TRIANGLE; a column out of range, a non-increasing row, a bad row_ptr
+ * -> DABS_E_ARG; the same int32 range check as dabs_create -> DABS_E_RANGE.
+ * The device keeps the same symmetric dense rows. */
+dabs_status dabs_create_csr(int32_t n, const int32_t* row_ptr, const int32_t* col, const int16_t* val,
+                            const int16_t* diag, const dabs_config* cfg, dabs_ctx** out);
+
 /* Reset to the start of a run: slots X=0, E=0, Delta_k=W_kk,
  * empty tabu rings; pools = random +inf sentinels drawn from `seed`
  * (R-19); generation 0. */

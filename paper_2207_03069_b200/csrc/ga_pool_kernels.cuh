@@ -66,6 +66,22 @@ __global__ void symmetrize_kernel(const int16_t* __restrict__ U, int n, int n_pa
     }
 }
 
+// CSR upper triangle -> symmetric dense rows (one CTA per row), diag, pads
+__global__ void csr_scatter_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                   const int16_t* __restrict__ val, const int16_t* __restrict__ dg, int n,
+                                   int n_pad, int16_t* __restrict__ W, int32_t* __restrict__ diag)
+{
+    const int i = blockIdx.x;
+    for (int e = rp[i] + threadIdx.x; e < rp[i + 1]; e += blockDim.x) {
+        const int j = col[e];
+        W[(size_t)i * n_pad + j] = val[e];
+        W[(size_t)j * n_pad + i] = val[e];
+    }
+    if (threadIdx.x == 0) diag[i] = dg[i];
+    if (i == 0)
+        for (int k = n + threadIdx.x; k < n_pad; k += blockDim.x) diag[k] = INT32_MAX;
+}
+
 // rmax[i] = max_{k != i} |W_ik| (one CTA per row): how far any Delta_k can
 // move in one flip of bit i (batch kernel's lower bound on min Delta)
 __global__ void rowmax_kernel(const int16_t* __restrict__ W, int n, int n_pad, int32_t* __restrict__ rmax)

@@ -187,12 +187,13 @@ static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
 }
 
 // ---------------------------------------------------------------- create
-extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg_in,
-                                   dabs_ctx** out)
+static void dabs_destroy_impl(dabs_ctx* c);
+
+// configuration, device, stream, tiling and GA constants common to both ingest paths
+static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx** out)
 {
     if (!out) return fail(DABS_E_ARG, "out is NULL");
     *out = nullptr;
-    if (!W_host) return fail(DABS_E_ARG, "W is NULL");
     if (n < 1 || n > 32768) return fail(DABS_E_ARG, "n=%d outside [1, 32768]", n);
     dabs_config cfg;
     dabs_config_default(&cfg);
@@ -212,7 +213,7 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
     dabs_ctx* c = new dabs_ctx();
     c->cfg = cfg;
     auto bail = [&](dabs_status st) {
-        dabs_destroy(c);
+        dabs_destroy_impl(c);
         return st;
     };
     int ndev = 0;
@@ -292,8 +293,15 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
     g.n_gen = 0; g.n_alg = 0;
     for (int k = 0; k < N_GEN; k++) if (cfg.genop_mask >> k & 1) g.gens[g.n_gen++] = k;
     for (int k = 0; k < N_ALG; k++) if (cfg.algo_mask >> k & 1) g.algs[g.n_alg++] = k;
+    *out = c;
+    return DABS_OK;
+}
 
-    // ---- a1: upload, check, symmetrize
+// a1 (dense): upload the host triangle, check it, build symmetric rows
+static dabs_status ingest_dense(dabs_ctx* c, const int16_t* W_host)
+{
+    const int n = c->n;
+    auto bail = [&](dabs_status st) { return st; };
     int16_t* U = nullptr;
     dabs_status st;
     if ((st = dalloc(c, &U, (size_t)n * n)) != DABS_OK) return bail(st);
@@ -329,6 +337,16 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
             break;
         }
 
+    return DABS_OK;
+}
+
+// tables, slots, packets, pools, exchange buffers
+static dabs_status create_end(dabs_ctx* c)
+{
+    const int n = c->n;
+    const dabs_config& cfg = c->cfg;
+    dabs_status st;
+    auto bail = [&](dabs_status st2) { return st2; };
     // ---- schedule tables for CyclicMin (R-7) and RandomMin (R-8)
     {
         std::vector<int32_t> wt(c->T + 1), pt(c->T + 1);
@@ -394,11 +412,90 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
 #undef AB
     c->best_X.assign(n, 0);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DABS_E_CUDA, "create: %s", cudaGetErrorString(cudaGetLastError())));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg_in,
+                                   dabs_ctx** out)
+{
+    if (!out) return fail(DABS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!W_host) return fail(DABS_E_ARG, "W is NULL");
+    dabs_ctx* c = nullptr;
+    dabs_status st = create_begin(n, cfg_in, &c);
+    if (st != DABS_OK) return st;
+    if ((st = ingest_dense(c, W_host)) != DABS_OK || (st = create_end(c)) != DABS_OK) {
+        const std::string msg = g_err;
+        dabs_destroy_impl(c);
+        g_err = msg;
+        return st;
+    }
     *out = c;
     return DABS_OK;
 }
 
-extern "C" void dabs_destroy(dabs_ctx* c)
+// a1 (CSR): validate the host upper-triangle CSR, upload it, scatter into the
+// same symmetric dense rows (the per-flip scan is O(n) whatever the storage)
+extern "C" dabs_status dabs_create_csr(int32_t n, const int32_t* row_ptr, const int32_t* col, const int16_t* val,
+                                       const int16_t* diag, const dabs_config* cfg_in, dabs_ctx** out)
+{
+    if (!out) return fail(DABS_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!row_ptr || !diag) return fail(DABS_E_ARG, "row_ptr / diag is NULL");
+    if (n < 1 || n > 32768) return fail(DABS_E_ARG, "n=%d outside [1, 32768]", n);
+    if (row_ptr[0] != 0) return fail(DABS_E_ARG, "row_ptr[0] != 0");
+    const int64_t nnz = row_ptr[n];
+    if (nnz < 0 || nnz > (int64_t)n * (n - 1) / 2) return fail(DABS_E_ARG, "bad nnz %lld", (long long)nnz);
+    if (nnz > 0 && (!col || !val)) return fail(DABS_E_ARG, "col / val is NULL");
+    std::vector<int64_t> absum(n, 0);
+    for (int i = 0; i < n; i++) {
+        if (row_ptr[i + 1] < row_ptr[i]) return fail(DABS_E_ARG, "row_ptr not monotone at row %d", i);
+        absum[i] += diag[i] < 0 ? -(int64_t)diag[i] : diag[i];
+        for (int32_t e = row_ptr[i]; e < row_ptr[i + 1]; e++) {
+            const int32_t j = col[e];
+            if (j >= n || j < 0) return fail(DABS_E_ARG, "column %d out of range in row %d", j, i);
+            if (j <= i) return fail(DABS_E_TRIANGLE, "entry (%d,%d) is not strictly above the diagonal", i, j);
+            if (e > row_ptr[i] && j <= col[e - 1]) return fail(DABS_E_ARG, "row %d columns not strictly increasing", i);
+            const int64_t a = val[e] < 0 ? -(int64_t)val[e] : val[e];
+            absum[i] += a;
+            absum[j] += a;
+        }
+    }
+    for (int i = 0; i < n; i++)
+        if (absum[i] >= INT32_MAX) return fail(DABS_E_RANGE, "row %d: sum |W| does not fit int32 Delta", i);
+    dabs_ctx* c = nullptr;
+    dabs_status st = create_begin(n, cfg_in, &c);
+    if (st != DABS_OK) return st;
+    auto fin = [&](dabs_status s2) {
+        const std::string msg = g_err;
+        dabs_destroy_impl(c);
+        g_err = msg;
+        return s2;
+    };
+    int32_t *d_rp = nullptr, *d_col = nullptr;
+    int16_t *d_val = nullptr, *d_diag = nullptr;
+    if ((st = dalloc(c, &d_rp, n + 1)) != DABS_OK || (st = dalloc(c, &d_col, nnz)) != DABS_OK ||
+        (st = dalloc(c, &d_val, nnz)) != DABS_OK || (st = dalloc(c, &d_diag, n)) != DABS_OK ||
+        (st = dalloc(c, &c->W, (size_t)n * c->n_pad)) != DABS_OK || (st = dalloc(c, &c->diag, c->n_pad)) != DABS_OK ||
+        (st = dalloc(c, &c->scratch64, 4)) != DABS_OK || (st = dalloc(c, &c->rmax, n)) != DABS_OK)
+        return fin(st);
+    cudaStream_t s0 = c->stream;
+    if (cudaMemcpyAsync(d_rp, row_ptr, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s0) != cudaSuccess ||
+        (nnz && cudaMemcpyAsync(d_col, col, 4 * (size_t)nnz, cudaMemcpyHostToDevice, s0) != cudaSuccess) ||
+        (nnz && cudaMemcpyAsync(d_val, val, 2 * (size_t)nnz, cudaMemcpyHostToDevice, s0) != cudaSuccess) ||
+        cudaMemcpyAsync(d_diag, diag, 2 * (size_t)n, cudaMemcpyHostToDevice, s0) != cudaSuccess ||
+        cudaMemsetAsync(c->W, 0, sizeof(int16_t) * (size_t)n * c->n_pad, s0) != cudaSuccess)
+        return fin(fail(DABS_E_CUDA, "CSR upload failed"));
+    csr_scatter_kernel<<<n, 128, 0, s0>>>(d_rp, d_col, d_val, d_diag, n, c->n_pad, c->W, c->diag);
+    rowmax_kernel<<<n, 256, 0, s0>>>(c->W, n, c->n_pad, c->rmax);
+    if (cudaStreamSynchronize(s0) != cudaSuccess)
+        return fin(fail(DABS_E_CUDA, "CSR scatter: %s", cudaGetErrorString(cudaGetLastError())));
+    if ((st = create_end(c)) != DABS_OK) return fin(st);
+    *out = c;
+    return DABS_OK;
+}
+
+static void dabs_destroy_impl(dabs_ctx* c)
 {
     if (!c) return;
     cudaSetDevice(c->dev);
@@ -410,6 +507,8 @@ extern "C" void dabs_destroy(dabs_ctx* c)
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
+
+extern "C" void dabs_destroy(dabs_ctx* c) { dabs_destroy_impl(c); }
 
 // ---------------------------------------------------------------- reset / generation
 extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)

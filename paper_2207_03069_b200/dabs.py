@@ -53,8 +53,8 @@ class dabs_stats(C.Structure):
 
 
 # every symbol include/dabs.h declares (checked by tests/test_abi.py)
-EXPORTS = ["dabs_config_default", "dabs_create", "dabs_reset", "dabs_generation", "dabs_run", "dabs_best",
-           "dabs_energy", "dabs_get_stats", "dabs_debug_batch", "dabs_read_slot", "dabs_read_pool",
+EXPORTS = ["dabs_config_default", "dabs_create", "dabs_create_csr", "dabs_reset", "dabs_generation", "dabs_run",
+           "dabs_best", "dabs_energy", "dabs_get_stats", "dabs_debug_batch", "dabs_read_slot", "dabs_read_pool",
            "dabs_read_packet", "dabs_read_stats_pool", "dabs_trace_enable", "dabs_trace_read",
            "dabs_last_error", "dabs_destroy"]
 
@@ -79,6 +79,8 @@ def load(path: str = LIB_PATH):
     L.dabs_config_default.restype = None
     L.dabs_create.argtypes = [P, i32, C.POINTER(dabs_config), C.POINTER(C.c_void_p)]
     L.dabs_create.restype = st
+    L.dabs_create_csr.argtypes = [i32, P, P, P, P, C.POINTER(dabs_config), C.POINTER(C.c_void_p)]
+    L.dabs_create_csr.restype = st
     L.dabs_reset.argtypes = [P, u64]
     L.dabs_reset.restype = st
     L.dabs_generation.argtypes = [P]
@@ -133,15 +135,23 @@ def config_default() -> dabs_config:
 class Solver:
     """One rank's DABS context over an upper-triangular int16 W (Eq.(2))."""
 
-    def __init__(self, W: np.ndarray, *, s_milli: int = 100, b_milli: int = 1000, tabu: int = 8,
-                 cap: int = 100, eps_ppm: int = 50000, genop_mask: int = 0xFF, algo_mask: int = 0x1F,
+    def __init__(self, W: np.ndarray | None, *, csr=None, s_milli: int = 100, b_milli: int = 1000,
+                 tabu: int = 8, cap: int = 100, eps_ppm: int = 50000, genop_mask: int = 0xFF, algo_mask: int = 0x1F,
                  pools: int = 1, slots: int = 0, target: int | None = None, time_limit_ns: int = 0,
                  rank: int = 0, world: int = 1, device: int = -1, stream=None, exchange=None):
         L = load()
-        W = np.ascontiguousarray(W, dtype=np.int16)
-        if W.ndim != 2 or W.shape[0] != W.shape[1]:
-            raise ValueError("W must be square")
-        self.n = W.shape[0]
+        if csr is None:
+            W = np.ascontiguousarray(W, dtype=np.int16)
+            if W.ndim != 2 or W.shape[0] != W.shape[1]:
+                raise ValueError("W must be square")
+            self.n = W.shape[0]
+        else:
+            rp, col, val, diag = csr
+            rp = np.ascontiguousarray(rp, dtype=np.int32)
+            col = np.ascontiguousarray(col, dtype=np.int32)
+            val = np.ascontiguousarray(val, dtype=np.int16)
+            diag = np.ascontiguousarray(diag, dtype=np.int16)
+            self.n = diag.size
         cfg = config_default()
         cfg.s_milli, cfg.b_milli, cfg.tabu_period, cfg.pool_capacity = s_milli, b_milli, tabu, cap
         cfg.eps_ppm, cfg.genop_mask, cfg.algo_mask = eps_ppm, genop_mask, algo_mask
@@ -156,11 +166,27 @@ class Solver:
             cfg.exchange = self._exchange_cb
         self.cfg = cfg
         h = C.c_void_p()
-        _check(L.dabs_create(_p(W), self.n, C.byref(cfg), C.byref(h)))
+        if csr is None:
+            _check(L.dabs_create(_p(W), self.n, C.byref(cfg), C.byref(h)))
+        else:
+            _check(L.dabs_create_csr(self.n, _p(rp), _p(col) if col.size else None,
+                                     _p(val) if val.size else None, _p(diag), C.byref(cfg), C.byref(h)))
         self.h = h
         st = self.stats()
         self.slots, self.pools, self.cap = st.slots, st.pools, st.cap
         self.T, self.B, self.n_pad, self.threads = st.T, st.B, st.n_pad, st.threads_per_search
+
+    @staticmethod
+    def to_csr(U: np.ndarray):
+        """Upper-triangular dense U -> (row_ptr, col, val, diag) for dabs_create_csr."""
+        U = np.asarray(U)
+        n = U.shape[0]
+        iu = np.triu(U, 1)
+        rows, cols = np.nonzero(iu)
+        rp = np.zeros(n + 1, np.int32)
+        np.add.at(rp, rows + 1, 1)
+        return np.cumsum(rp).astype(np.int32), cols.astype(np.int32), iu[rows, cols].astype(np.int16), \
+            np.diag(U).astype(np.int16)
 
     def close(self):
         if getattr(self, "h", None):

@@ -255,3 +255,31 @@ def test_r32k_sampled_parity(orc, lib):
     np.testing.assert_array_equal(st.delta, post["delta"])
     # property at any size: E(BEST) equals Eq.(2) evaluated directly on the device
     assert solver.energy(pk["best"]) == pk["ebest"]
+
+
+def test_csr_ingest_equals_dense(orc, lib):
+    """dabs_create_csr builds the same device rows as dabs_create:
+    identical generations; its input checks report the documented errors."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, _, _ = wl.gset_like(300, 2000, seed=4)
+    csr = lib.Solver.to_csr(U)
+    a = lib.Solver(U, pools=2, slots=5, cap=16)
+    b = lib.Solver(None, csr=csr, pools=2, slots=5, cap=16)
+    for s_ in (a, b):
+        s_.reset(3)
+        for _ in range(3):
+            s_.generation()
+    for p in range(3):
+        np.testing.assert_array_equal(a.read_pool(p)["X"], b.read_pool(p)["X"])
+        np.testing.assert_array_equal(a.read_pool(p)["E"], b.read_pool(p)["E"])
+    x = np.random.default_rng(0).integers(0, 2, 300).astype(np.uint8)
+    assert a.energy(x) == b.energy(x) == orc.energy(U, x)
+    rp, col, val, diag = csr
+    bad = col.copy()
+    bad[0] = 0                                  # row 0 column 0: not above the diagonal
+    with pytest.raises(lib.DabsError, match="E_TRIANGLE"):
+        lib.Solver(None, csr=(rp, bad, val, diag))
+    bad = col.copy()
+    bad[1] = bad[0]                             # duplicate column in row 0
+    with pytest.raises(lib.DabsError, match="E_ARG"):
+        lib.Solver(None, csr=(rp, bad, val, diag))
