@@ -5,6 +5,7 @@
 // batch kernel's per-flip chain.
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -55,9 +56,12 @@ __global__ void rows(const char* W, size_t row_bytes, int n, int iters, int infl
     }
 }
 
-int main()
+int main(int argc, char** argv)
 {
-    const int n = 32768;
+    // rowbench [n] [max_ctas_per_sm]: n = 32768 streams 2 GiB from HBM; n = 2048
+    // keeps the 8 MiB matrix in L2 (the K2000s-class workloads)
+    const int n = argc > 1 ? atoi(argv[1]) : 32768;
+    const int max_per_sm = argc > 2 ? atoi(argv[2]) : 2;
     const size_t row = 2 * (size_t)n;
     char* W;
     cudaMalloc(&W, row * n);
@@ -72,7 +76,7 @@ int main()
     cudaEventCreate(&b);
     const int iters = 2000;
     for (int inflight = 1; inflight <= 2; inflight++)
-        for (int per_sm = 1; per_sm <= 2; per_sm++) {
+        for (int per_sm = 1; per_sm <= max_per_sm; per_sm *= 2) {
             const int grid = sms * per_sm;
             rows<<<grid, 32, 2 * row>>>(W, row, n, 50, inflight, sink);
             cudaEventRecord(a);
@@ -82,8 +86,9 @@ int main()
             float ms;
             cudaEventElapsedTime(&ms, a, b);
             const double bytes = (double)grid * iters * row;
-            printf("{\"rows_in_flight_per_cta\": %d, \"ctas_per_sm\": %d, \"GBps\": %.1f, \"us_per_row_per_cta\": %.3f}\n",
-                   inflight, per_sm, bytes / ms / 1e6, ms * 1e3 / iters);
+            printf("{\"n\": %d, \"row_bytes\": %zu, \"rows_in_flight_per_cta\": %d, \"ctas_per_sm\": %d, "
+                   "\"GBps\": %.1f, \"us_per_row_per_cta\": %.3f}\n",
+                   n, row, inflight, per_sm, bytes / ms / 1e6, ms * 1e3 / iters);
         }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
