@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdabs.so")
+LIB_PATH = os.environ.get("DABS_LIB", os.path.join(HERE, "libdabs.so"))   # DABS_LIB: A/B builds
 
 DABS_OK = 0
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_TRIANGLE", 3: "E_RANGE", 4: "E_NOMEM", 5: "E_CUDA", 6: "E_COMM",
