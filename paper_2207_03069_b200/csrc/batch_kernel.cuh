@@ -263,9 +263,10 @@ __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_
     return est;
 }
 
-template <int C, bool MW, bool TRACE>
-__global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams p)
+template <int C, int NTT, bool TRACE>
+__global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
 {
+    constexpr bool MW = NTT > 32;                    // more than one warp per search
     constexpr int EPT = 8 * C;
     constexpr int NP = MW ? (C >= 4 ? 4 : C) : 1;   // row pieces, one mbarrier each
     constexpr int CPP = C / NP;                      // chunks per piece
@@ -275,9 +276,10 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
     constexpr bits_t ALL = ~(bits_t)0;
     constexpr unsigned FULL = 0xffffffffu;
     const int t = threadIdx.x;
-    const int NT = MW ? (int)blockDim.x : 32;
-    const int lgNT = MW ? 31 - __clz(NT) : 5;
-    const int lane = t & 31, wid = t >> 5, NW = NT >> 5;
+    constexpr int NT = NTT;                          // threads per search (compile time)
+    constexpr int lgNT = NT == 32 ? 5 : NT == 64 ? 6 : NT == 128 ? 7 : NT == 256 ? 8 : 9;
+    constexpr int NW = NT >> 5;
+    const int lane = t & 31, wid = t >> 5;
     const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
     const int n = p.n;
@@ -821,7 +823,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
                 bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
         }
         E += sv;
-        glb = min(glb - (int64_t)p.rmax[si], (int64_t)-sv);
+        const int rmax_si = p.rmax[si];   // consumed after the update: its latency hides there
         // sigma(x_i) = -1 (x_i = 0 before the flip): negate every sigma(x_k) byte
         const uint32_t cmask = sx ? 0u : 0xFEFEFEFEu;
         if (__any_sync(FULL, owns(si))) {
@@ -900,6 +902,7 @@ __global__ void __launch_bounds__(MW ? 512 : 32) batch_kernel(const BatchParams 
             }
         }
         par_row ^= 1u;
+        glb = min(glb - (int64_t)rmax_si, (int64_t)-sv);
     }
 
     // ---------------- write back state and the result packet

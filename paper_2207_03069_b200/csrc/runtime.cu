@@ -151,14 +151,21 @@ static int flip_factor(uint32_t milli, int n)
 // ---------------------------------------------------------------- kernels by tier
 using BatchFn = void (*)(const BatchParams);
 
-static BatchFn pick_batch(int C, bool mw, bool trace)
+static BatchFn pick_batch(int C, int NT, bool trace)
 {
-    if (mw) return trace ? batch_kernel<8, true, true> : batch_kernel<8, true, false>;
+    if (NT > 32) {
+        switch (NT) {
+        case 64: return trace ? batch_kernel<8, 64, true> : batch_kernel<8, 64, false>;
+        case 128: return trace ? batch_kernel<8, 128, true> : batch_kernel<8, 128, false>;
+        case 256: return trace ? batch_kernel<8, 256, true> : batch_kernel<8, 256, false>;
+        default: return trace ? batch_kernel<8, 512, true> : batch_kernel<8, 512, false>;
+        }
+    }
     switch (C) {
-    case 1: return trace ? batch_kernel<1, false, true> : batch_kernel<1, false, false>;
-    case 2: return trace ? batch_kernel<2, false, true> : batch_kernel<2, false, false>;
-    case 4: return trace ? batch_kernel<4, false, true> : batch_kernel<4, false, false>;
-    default: return trace ? batch_kernel<8, false, true> : batch_kernel<8, false, false>;
+    case 1: return trace ? batch_kernel<1, 32, true> : batch_kernel<1, 32, false>;
+    case 2: return trace ? batch_kernel<2, 32, true> : batch_kernel<2, 32, false>;
+    case 4: return trace ? batch_kernel<4, 32, true> : batch_kernel<4, 32, false>;
+    default: return trace ? batch_kernel<8, 32, true> : batch_kernel<8, 32, false>;
     }
 }
 
@@ -263,7 +270,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     c->n_pad = c->NT * c->C * 8;
     c->nwp = c->n_pad / 32;
     for (int tr = 0; tr < 2; tr++) {
-        cudaError_t e = cudaFuncSetAttribute(pick_batch(c->C, c->mw, tr != 0),
+        cudaError_t e = cudaFuncSetAttribute(pick_batch(c->C, c->NT, tr != 0),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
@@ -276,7 +283,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         c->S = (int)cfg.slots_per_pool;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->mw, false), c->NT, row_smem(c));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->NT, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = prop.multiProcessorCount * occ;
         c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
@@ -545,7 +552,7 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
 {
     BatchParams p = batch_params(c, seed, gen, slot0);
     p.order = order;
-    BatchFn fn = pick_batch(c->C, c->mw, trace);
+    BatchFn fn = pick_batch(c->C, c->NT, trace);
     fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
     CK(cudaGetLastError());
     return DABS_OK;
