@@ -139,6 +139,49 @@ def euclid_tsp(m: int = 32, seed: int = 1):
     return qap_qubo(circular_flow(m), d, p), d, p
 
 
+def ising_to_qubo(n: int, J_edges: np.ndarray, J: np.ndarray, h: np.ndarray):
+    """Ising -> QUBO with s = 2x - 1 (constructive form SPEC S:69):
+    U_ij = 4 J_ij (i < j), U_ii = 2 h_i - 2 sum_j J_ij, offset = sum J - sum h, so
+    E(X) + offset = H(S) for every spin vector (Eq.(1)).  Returns (U, offset)."""
+    U = np.zeros((n, n), np.int64)
+    i = np.minimum(J_edges[:, 0], J_edges[:, 1])
+    j = np.maximum(J_edges[:, 0], J_edges[:, 1])
+    np.add.at(U, (i, j), 4 * J)
+    d = 2 * h.astype(np.int64)
+    np.add.at(d, i, -2 * J)
+    np.add.at(d, j, -2 * J)
+    U[np.arange(n), np.arange(n)] += d
+    assert np.abs(U).max() <= 32767
+    return U.astype(np.int16), int(J.sum() - h.sum())
+
+
+def qasp_like(n: int = 5627, m: int = 40279, r: int = 1, seed: int = 1):
+    """QASP-shaped sparse Ising: a synthetic stand-in for
+    the D-Wave Advantage 4.1 working graph (5627 nodes, 40279 edges; the real
+    faulty-qubit graph is not available): local random edges (each node links to
+    nodes within a window of +-64 positions, like Pegasus' bounded degree ~14),
+    J uniform over the 2r nonzero integers of [-r, r], h over the 8r nonzero
+    integers of [-4r, 4r].  Returns (U, offset, edges, J, h)."""
+    rng = _rng(seed)
+    seen = set()
+    edges = []
+    while len(edges) < m:
+        a = int(rng.integers(0, n))
+        b = int((a + rng.integers(1, 65)) % n)
+        key = (min(a, b), max(a, b))
+        if key in seen:
+            continue
+        seen.add(key)
+        edges.append(key)
+    edges = np.array(edges, np.int64)
+    Jv = np.concatenate([np.arange(-r, 0), np.arange(1, r + 1)])
+    hv = np.concatenate([np.arange(-4 * r, 0), np.arange(1, 4 * r + 1)])
+    J = rng.choice(Jv, size=m)
+    h = rng.choice(hv, size=n)
+    U, off = ising_to_qubo(n, edges, J, h)
+    return U, off, edges, J, h
+
+
 def random_target(n: int, seed: int) -> np.ndarray:
     return _rng(seed).integers(0, 2, size=n, dtype=np.uint8)
 
@@ -159,4 +202,8 @@ def make(config: str, seed: int = 1):
         return U, dict(s_milli=100, b_milli=10000)
     if config == "R32K":
         return random_dense(32768, seed), dict(s_milli=100, b_milli=1000)
+    if config.startswith("QASP"):               # QASP1 / QASP16 / QASP256 (resolution r)
+        r = int(config[4:] or 1)
+        U, off, _, _, _ = qasp_like(5627, 40279, r, seed)
+        return U, dict(s_milli=100, b_milli=1000, offset=off, sparse=True)
     raise KeyError(config)

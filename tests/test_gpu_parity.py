@@ -283,3 +283,26 @@ def test_csr_ingest_equals_dense(orc, lib):
     bad[1] = bad[0]                             # duplicate column in row 0
     with pytest.raises(lib.DabsError, match="E_ARG"):
         lib.Solver(None, csr=(rp, bad, val, diag))
+
+
+def test_qasp_sampled_parity(orc, lib):
+    """QASP-shaped sparse Ising through dabs_create_csr, bench
+    launch configuration: sampled slots of generation 1 recomputed by the oracle."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("QASP16", seed=1)
+    solver = lib.Solver(None, csr=lib.Solver.to_csr(U), s_milli=meta["s_milli"], b_milli=meta["b_milli"])
+    solver.reset(5)
+    solver.generation()
+    sample = [0, solver.slots // 3, solver.slots - 1]
+    pre = {s: solver.read_slot(s) for s in sample}
+    solver.generation()
+    for s in sample:
+        pk = solver.read_packet(s)
+        post = solver.read_slot(s)
+        st = orc.SlotState(pre[s]["x"].copy(), pre[s]["delta"].copy(), pre[s]["E"], pre[s]["ring"].copy())
+        ref = orc.batch(U, st, pk["D"], pk["algo"], T=solver.T, B=solver.B, tabu=8, seed=5, slot=s, gen=1)
+        assert ref.flips == pk["flips"] and ref.ebest == pk["ebest"]
+        np.testing.assert_array_equal(ref.best, pk["best"])
+        np.testing.assert_array_equal(st.delta, post["delta"])
+    E, x = solver.best()
+    assert solver.energy(x) == E == orc.energy(U, x)

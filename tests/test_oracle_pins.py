@@ -610,3 +610,27 @@ def test_randommin_draws_uniform(orc):
     assert np.abs(hist - 1 / 16).max() < 0.01
     xs = [orc.lowbias32(x) for x in range(0, 1 << 16)]
     assert len(set(xs)) == len(xs)
+
+
+def test_ising_to_qubo_exhaustive(orc):
+    """Ising -> QUBO: E(X) + offset = H(S) for every spin vector of
+    random Ising models (H from Eq.(1) directly), and the QASP generator's
+    value ranges."""
+    from paper_2207_03069_b200 import workloads as wl
+    rng = np.random.default_rng(23)
+    for _ in range(20):
+        n = int(rng.integers(2, 10))
+        pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
+        m = int(rng.integers(1, len(pairs) + 1))
+        edges = np.array([pairs[k] for k in rng.choice(len(pairs), m, replace=False)], np.int64)
+        J = rng.choice([-3, -2, -1, 1, 2, 3], m)
+        h = rng.integers(-12, 13, n)
+        U, off = wl.ising_to_qubo(n, edges, J, h)
+        for x in all_x(n):
+            s = 2 * x - 1
+            H = sum(int(Jk) * s[a] * s[b] for (a, b), Jk in zip(edges, J)) + int((h * s).sum())
+            assert orc.energy(U, x) + off == H
+    U, off, edges, J, h = wl.qasp_like(300, 2000, r=16, seed=2)
+    assert len(edges) == 2000 and len({tuple(e) for e in edges.tolist()}) == 2000
+    assert set(np.unique(np.abs(J))) <= set(range(1, 17)) and 0 not in J
+    assert np.abs(h).max() <= 64 and 0 not in h
