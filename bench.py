@@ -6,7 +6,7 @@ of every slot, one batch search per slot (Straight, Greedy, main rounds), pool
 merge, exchange.  `value` = box-wide flips in the K timed steps / device time
 (CUDA events on the library's stream, max over ranks).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload R32K|K2000s|TSP32|GS800|K16]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload R32K|R64K|K2000s|TSP32|GS800|K16|QASP*]
     python bench.py --impl reference ...   # the CPU oracle on the host cores
 
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; one rank per GPU,
@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dabs", choices=["dabs", "reference"])
     ap.add_argument("--workload", default="R32K",
-                    choices=["K16", "GS800", "TSP32", "K2000s", "R32K", "QASP1", "QASP16", "QASP256"])
+                    choices=["K16", "GS800", "TSP32", "K2000s", "R32K", "R64K", "QASP1", "QASP16", "QASP256"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--slots", type=int, default=0, help="slots per pool (0 = library default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample size (cpu_baseline)")

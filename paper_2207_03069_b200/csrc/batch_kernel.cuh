@@ -15,6 +15,11 @@
 //
 // MW=false: one warp per search (n <= 2048), no CTA barriers at all.
 // MW=true : NT in {64..512} threads per search (n <= 32768).
+// CL=2    : a cluster of two CTAs of NT threads per search (n <= 65536,
+//           SURVEY 8(f) f2).  Each CTA holds half of every chunk (thread
+//           tq = rank*NT + t of the search's 2*NT), streams its half of the
+//           row, and every CTA-wide reduction is completed by one DSMEM swap
+//           with the peer CTA (cl_swap).
 //
 // Citations: P:n = PAPER.md line n; R-x = DESIGN.md readings.
 #pragma once
@@ -92,6 +97,79 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity)
         : "memory");
 }
 
+// expect `bytes` more on mbarrier m (the copies that deliver them follow)
+__device__ __forceinline__ void mbar_expect(uint64_t* m, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* m)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(m))
+        : "memory");
+}
+
+// ---- thread-block cluster (CL = 2 CTAs per search, DSMEM exchange)
+__device__ __forceinline__ uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t addr, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_peer(uint32_t addr, int v)
+{
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_peer(uint32_t addr)
+{
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* m, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Swap K uniform values with the peer CTA of the cluster.  Thread 0 stores them
+// into the peer's xv[par] and arrives (release.cluster) on the peer's xbar[par];
+// every thread waits (acquire.cluster) on its own xbar[par].  Callers reach
+// this right after a __syncthreads, so the peer can only reuse xv[par] (two
+// swaps later) once every thread here has read it.
+template <int K>
+__device__ __forceinline__ void cl_swap(const int (&mine)[K], int (&theirs)[K], int32_t (*xv)[8], uint64_t* xbar,
+                                        int& xc, uint32_t peer, int t)
+{
+    const int par = xc & 1;
+    const uint32_t ph = (uint32_t)(xc >> 1) & 1u;
+    xc++;
+    if (t == 0) {
+        const uint32_t base = mapa_peer(smem_u32(&xv[par][0]), peer);
+#pragma unroll
+        for (int k = 0; k < K; k++) st_peer(base + 4u * k, mine[k]);
+        mbar_arrive_peer(mapa_peer(smem_u32(&xbar[par]), peer));
+    }
+    mbar_wait_cluster(&xbar[par], ph);
+#pragma unroll
+    for (int k = 0; k < K; k++) theirs[k] = xv[par][k];
+}
+
 enum : int { OP_MIN = 0, OP_MAX = 1, OP_ADD = 2, OP_OR = 3 };
 
 __device__ __forceinline__ int wop(int op, int v)
@@ -101,6 +179,15 @@ __device__ __forceinline__ int wop(int op, int v)
     case OP_MAX: return warp_max(v);
     case OP_ADD: return (int)warp_add((unsigned)v);
     default: return (int)warp_or((unsigned)v);
+    }
+}
+__device__ __forceinline__ int op2(int op, int a, int b)
+{
+    switch (op) {
+    case OP_MIN: return min(a, b);
+    case OP_MAX: return max(a, b);
+    case OP_ADD: return a + b;
+    default: return a | b;
     }
 }
 __device__ __forceinline__ int op_ident(int op)
@@ -263,9 +350,10 @@ __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_
     return est;
 }
 
-template <int C, int NTT, bool TRACE>
-__global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
+template <int C, int NTT, int CL, bool TRACE>
+__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 1) batch_kernel(const BatchParams p)
 {
+    static_assert(CL == 1 || (CL == 2 && NTT > 32), "cluster tier needs the CTA tier");
     constexpr bool MW = NTT > 32;                    // more than one warp per search
     constexpr int EPT = 8 * C;
     constexpr int NP = MW ? (C >= 4 ? 4 : C) : 1;   // row pieces, one mbarrier each
@@ -278,20 +366,30 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
     const int t = threadIdx.x;
     constexpr int NT = NTT;                          // threads per search (compile time)
     constexpr int lgNT = NT == 32 ? 5 : NT == 64 ? 6 : NT == 128 ? 7 : NT == 256 ? 8 : 9;
+    constexpr int NTG = NT * CL;                     // threads of the whole search
+    constexpr int lgNTG = lgNT + (CL == 2 ? 1 : 0);
     constexpr int NW = NT >> 5;
     const int lane = t & 31, wid = t >> 5;
-    const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
+    const uint32_t rank = CL == 2 ? cluster_rank() : 0u;   // CTA within the search's cluster
+    const int tq = (int)rank * NT + t;                      // thread within the search
+    const int sidx = (int)blockIdx.x / CL;
+    const int s = p.order ? p.order[sidx] : p.slot0 + sidx;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
     const int n = p.n;
 
     extern __shared__ __align__(128) uint8_t dyn_smem[];
-    const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // one W row, 2*n_pad bytes
-    uint8_t* tcnt = dyn_smem + 2 * p.n_pad;   // per element: occurrences in the last `tabu` flips
+    const int nl = p.n_pad / CL;              // elements held by this CTA
+    const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // this CTA's part of a W row, 2*nl bytes
+    uint8_t* tcnt = dyn_smem + 2 * nl;        // per local element: occurrences in the last `tabu` flips
     __shared__ __align__(8) uint64_t mbar[NP];
     __shared__ int32_t ring_s[TABU_RING];
     __shared__ int32_t red_s[2][32][RED_W];
     __shared__ int32_t bc_s[2][4];
     __shared__ int32_t sel_s[4];   // MaxMin/PositiveMin pick, published through the row mbarrier
+    __shared__ int32_t xv_s[2][8];                 // CL = 2: the peer CTA's values of a swap
+    __shared__ __align__(8) uint64_t xbar[2];
+    int xc = 0;
+    const uint32_t peer = rank ^ 1u;
 
     // ---------------- load the slot's persistent state (R-14)
     int32_t d[EPT];
@@ -302,7 +400,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
         const int32_t* dp = p.delta + (size_t)s * p.n_pad;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const int ch = (c << lgNT) + t;
+            const int ch = (c << lgNTG) + tq;
             xb |= (bits_t)Xb[ch] << (8 * c);
             db |= (bits_t)Db[ch] << (8 * c);
             const int nv = min(max(n - ch * 8, 0), 8);
@@ -318,7 +416,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
     // Registers for one warp per search; shared memory ([EPT/16][NT] uint4,
     // conflict-free) for the CTA tier, where registers are the limit.
     uint32_t sg[MW ? 1 : EPT / 4];
-    uint4* sgs = reinterpret_cast<uint4*>(dyn_smem + 3 * p.n_pad);
+    uint4* sgs = reinterpret_cast<uint4*>(dyn_smem + 3 * nl);
 #pragma unroll
     for (int g = 0; g < EPT / 4; g++) {
         uint32_t w = 0;
@@ -331,6 +429,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
     if (t == 0) {
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) mbar_init(&mbar[qq], 1);
+        if constexpr (CL == 2) { mbar_init(&xbar[0], 1); mbar_init(&xbar[1], 1); }
         fence_mbar_init();
     }
     int pos = 0;   // ring_s[(pos + j) & 31] = j-th most recent flip
@@ -342,17 +441,50 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
     // the last `tabu` flips (shared memory) and keeps the bits count > 0 in tm
 #pragma unroll
     for (int c = 0; c < C; c++) reinterpret_cast<uint2*>(tcnt)[(c << lgNT) + t] = make_uint2(0u, 0u);
-    const uint32_t piece_bytes = (uint32_t)(2 * p.n_pad / NP);
+    const uint32_t piece_bytes = (uint32_t)(2 * nl / NP);
     uint32_t par_row = 0;
     int flips = 0;
     int64_t ebest = E_INF;
     bits_t bdiff = 0;              // BEST = X xor bdiff
     int rc = 0;                    // exchange parity counter
-    if constexpr (MW) __syncthreads(); else __syncwarp();
+    if constexpr (CL == 2) cluster_sync_all();      // the peer's barriers exist before any swap
+    else if constexpr (MW) __syncthreads();
+    else __syncwarp();
 
-    auto gidx = [&](int c, int e) { return (((c << lgNT) + t) << 3) | e; };
-    auto owns = [&](int k) { return ((k >> 3) & (NT - 1)) == t; };
-    auto lbit = [&](int k) { return (((k >> 3) >> lgNT) << 3) | (k & 7); };
+    auto gidx = [&](int c, int e) { return (((c << lgNTG) + tq) << 3) | e; };
+    auto owns = [&](int k) { return ((k >> 3) & (NTG - 1)) == tq; };
+    auto lbit = [&](int k) { return (((k >> 3) >> lgNTG) << 3) | (k & 7); };
+    // shared-memory index of an owned element (= k for CL = 1)
+    auto lidx = [&](int k) { return (((k >> 3) >> lgNTG) << (lgNT + 3)) | (t << 3) | (k & 7); };
+    // start the copy of this CTA's part of row i (every chunk's NT*8 elements)
+    auto issue_row = [&](int i) {
+        fence_proxy_async();
+        const char* src = reinterpret_cast<const char*>(p.W) + (size_t)i * (size_t)(2 * p.n_pad);
+#pragma unroll
+        for (int qq = 0; qq < NP; qq++) {
+            if constexpr (CL == 1) {
+                bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
+            } else {
+                mbar_expect(&mbar[qq], piece_bytes);
+#pragma unroll
+                for (int cc = 0; cc < CPP; cc++) {
+                    const int c = qq * CPP + cc;
+                    bulk_copy(dyn_smem + ((size_t)c << (lgNT + 4)), src + ((size_t)((c << lgNTG) + (int)rank * NT) << 4),
+                              (uint32_t)(NT * 16), &mbar[qq]);
+                }
+            }
+        }
+    };
+    // complete a CTA-wide reduction over the cluster (CL = 2; no-op otherwise)
+    auto cl_combine = [&](auto& v, const auto& ops) {
+        if constexpr (CL == 2) {
+            constexpr int K = sizeof(ops) / sizeof(ops[0]);
+            int o[K];
+            cl_swap<K>(v, o, xv_s, xbar, xc, peer, t);
+#pragma unroll
+            for (int k = 0; k < K; k++) v[k] = op2(ops[k], v[k], o[k]);
+        }
+    };
 
     // phases: 0 Straight, 1 Greedy, 2 main (R-12)
     int phase = 0, round = 0, tt = 0, cursor = 0;
@@ -373,7 +505,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
         bits_t cand = 0;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const uint32_t j0 = (uint32_t)(((c << lgNT) + t) << 2);   // first pair of the chunk
+            const uint32_t j0 = (uint32_t)(((c << lgNTG) + tq) << 2);   // first pair of the chunk
             uint32_t byte = 0;
 #pragma unroll
             for (int h = 0; h < 4; h++) {
@@ -390,7 +522,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
     uint4 r_pre = make_uint4(0, 0, 0, 0);
     for (int j = 0; j < tabu; j++) {
         const int r = ring_s[j];
-        if (r >= 0 && owns(r)) { tcnt[r]++; tm |= ONE << lbit(r); }
+        if (r >= 0 && owns(r)) { tcnt[lidx(r)]++; tm |= ONE << lbit(r); }
     }
 
     while (true) {
@@ -422,7 +554,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
 #pragma unroll
                 for (int c = 0; c < C; c++) {
                     // uniform: does the window meet chunk c at all (its span is NT*8 elements)?
-                    const int s0 = (c << lgNT) << 3, s1 = s0 + (NT << 3);
+                    const int s0 = (c << lgNTG) << 3, s1 = s0 + (NTG << 3);
                     if ((cursor < s1 && b0 > s0) || b1 > s0) {
                         const int base = gidx(c, 0);
                         const int lo = max(cursor - base, 0), hi = min(b0 - base, 8);
@@ -511,6 +643,15 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                 m = warp_min(a);
                 key = warp_min(a == m ? b : INT32_MAX);
                 gmin = warp_min(c2);
+                if constexpr (CL == 2) {
+                    const int mine[3] = {m, key, gmin};
+                    int o[3];
+                    cl_swap<3>(mine, o, xv_s, xbar, xc, peer, t);
+                    const int m2 = min(m, o[0]);
+                    key = min(m == m2 ? key : INT32_MAX, o[0] == m2 ? o[1] : INT32_MAX);
+                    m = m2;
+                    gmin = min(gmin, o[2]);
+                }
             } else {
                 m = wmin;
                 key = k;
@@ -530,12 +671,14 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                 int v2[1] = {t2};
                 const int ops1[1] = {OP_MIN};
                 block_reduce<MW>(v2, ops1, red_s, rc, lane, wid, NW);
+                cl_combine(v2, ops1);
                 bits_t MM = M2;
                 if (v2[0] == INT32_MAX) {
                     if (skip_g) {                   // exact global minimum needed after all
                         tg = min_all(d);
                         int v3[1] = {tg};
                         block_reduce<MW>(v3, ops1, red_s, rc, lane, wid, NW);
+                        cl_combine(v3, ops1);
                         gmin = v3[0];
                     }
                     MM = vb; t2 = tg; v2[0] = gmin;
@@ -554,6 +697,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                     }
                 int kv[1] = {k2};
                 block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
+                cl_combine(kv, ops1);
                 key = kv[0];
             }
             si = key >> 1;
@@ -579,6 +723,14 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
             if constexpr (MW) {
                 ov = bc_s[(rc - 1) & 1][0];
                 ox = bc_s[(rc - 1) & 1][1];
+                if constexpr (CL == 2) {
+                    // the owner of fixed_i is in one CTA of the two
+                    const bool own_cta = (((fixed_i >> 3) & (NTG - 1)) >> lgNT) == (int)rank;
+                    int w3[3] = {v[0], own_cta ? ov : 0, own_cta ? ox : 0};
+                    const int ops3[3] = {OP_MIN, OP_ADD, OP_ADD};
+                    cl_combine(w3, ops3);
+                    v[0] = w3[0]; ov = w3[1]; ox = w3[2];
+                }
             } else {
                 const int src = (fixed_i >> 3) & 31;
                 ov = __shfl_sync(FULL, ov, src);
@@ -627,6 +779,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
             int v[4] = {tg, a1, a2, el != 0};
             const int ops[4] = {OP_MIN, OP_MIN, OP_MAX, OP_OR};
             block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
+            cl_combine(v, ops);
             gmin = v[0];
             bits_t EL = el;
             int thr;
@@ -645,6 +798,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                 int w2[2] = {b1, b2 < 0x7FFFFFFEu ? (int)b2 + 1 : INT32_MAX};
                 const int ops2[2] = {OP_MAX, OP_MIN};
                 block_reduce<MW>(w2, ops2, red_s, rc, lane, wid, NW);
+                cl_combine(w2, ops2);
                 v[1] = algo == ALG_MAXMIN ? gmin : w2[1];
                 v[2] = w2[0];
             }
@@ -701,19 +855,45 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                 for (int w = 0; w < CW; w++) bt[w] = wt[w];
             }
             // chunk-major order: chunk 0 of all threads, then chunk 1, ...
+            // (CL = 2: within a chunk, CTA 0's threads come before CTA 1's)
+            uint32_t bo[CW];                      // the peer CTA's counts
+#pragma unroll
+            for (int w = 0; w < CW; w++) bo[w] = 0;
+            if constexpr (CL == 2) {
+                int mine[CW], o[CW];
+#pragma unroll
+                for (int w = 0; w < CW; w++) mine[w] = (int)bt[w];
+                cl_swap<CW>(mine, o, xv_s, xbar, xc, peer, t);
+#pragma unroll
+                for (int w = 0; w < CW; w++) bo[w] = (uint32_t)o[w];
+            }
             uint32_t tot = 0;
 #pragma unroll
-            for (int c = 0; c < C; c++) tot += (bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+            for (int c = 0; c < C; c++)
+                tot += ((bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu) + ((bo[c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
             int r1 = (int)pick_u(u, tot);
             int cs = 0;
 #pragma unroll
             for (int c = 0; c < C; c++) {
-                const int tc = (int)((bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
+                const int tc = (int)(((bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu) + ((bo[c >> 1] >> (16 * (c & 1))) & 0xFFFFu));
                 if (cs == c && r1 >= tc) { r1 -= tc; cs = c + 1; }
             }
+            bool locate = true;                   // does this CTA hold rank r1 of chunk cs?
+            if constexpr (CL == 2) {
+                uint32_t mc = 0, oc = 0;
+#pragma unroll
+                for (int c = 0; c < C; c++)
+                    if (c == cs) {
+                        mc = (bt[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                        oc = (bo[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+                    }
+                const int c0 = (int)(rank == 0 ? mc : oc);
+                if (rank == 0) locate = r1 < c0;
+                else { locate = r1 >= c0; r1 -= c0; }
+            }
             // which warp holds rank r1 of chunk cs
-            int wsel = 0;
-            if constexpr (MW) {
+            int wsel = locate ? 0 : -1;
+            if (MW && locate) {
                 int x = lane < NW ? (int)(((uint32_t)red_s[par][lane][cs >> 1] >> (16 * (cs & 1))) & 0xFFFFu) : 0;
                 int y = x;
 #pragma unroll
@@ -752,17 +932,20 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                     lx = (int)((xb >> li) & 1);
                 }
             }
-            if constexpr (MW) {
+            if constexpr (CL == 2) {
+                // the pick is in one CTA: one more reduction + swap makes it uniform
+                int q3[3] = {gi, gi >= 0 ? lv : 0, gi >= 0 ? lx : 0};
+                const int ops3[3] = {OP_MAX, OP_ADD, OP_ADD};
+                block_reduce<MW>(q3, ops3, red_s, rc, lane, wid, NW);
+                cl_combine(q3, ops3);
+                si = q3[0]; sv = q3[1]; sx = q3[2];
+            } else if constexpr (MW) {
                 // the locating thread publishes the pick and starts the row copy
                 // itself; everybody else learns (i, Delta_i, x_i) from the row's
                 // mbarrier (arrive = release, try_wait = acquire): no CTA barrier
                 if (gi >= 0) {
                     sel_s[0] = gi; sel_s[1] = lv; sel_s[2] = lx;
-                    fence_proxy_async();
-                    const char* src = reinterpret_cast<const char*>(p.W) + (size_t)gi * (size_t)(2 * p.n_pad);
-#pragma unroll
-                    for (int qq = 0; qq < NP; qq++)
-                        bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
+                    issue_row(gi);
                 }
             } else {
                 const int src = __ffs(__ballot_sync(FULL, gi >= 0)) - 1;
@@ -794,6 +977,7 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
                 int kv[1] = {k3};
                 const int ops1[1] = {OP_MIN};
                 block_reduce<MW>(kv, ops1, red_s, rc, lane, wid, NW);
+                cl_combine(kv, ops1);
                 bk = kv[0];
             }
             ebest = E + gmin;
@@ -811,16 +995,12 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
 
         // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
         // every thread has passed the last exchange: the row buffer is free
-        const bool pre_issued = MW && kind == 1;
+        const bool pre_issued = MW && CL == 1 && kind == 1;
         if (pre_issued) {
             mbar_wait(&mbar[0], par_row);
             si = sel_s[0]; sv = sel_s[1]; sx = sel_s[2];
         } else if (t == 0) {
-            fence_proxy_async();
-            const char* src = reinterpret_cast<const char*>(p.W) + (size_t)si * (size_t)(2 * p.n_pad);
-#pragma unroll
-            for (int qq = 0; qq < NP; qq++)
-                bulk_row_piece(dyn_smem + qq * piece_bytes, src + qq * piece_bytes, piece_bytes, &mbar[qq]);
+            issue_row(si);
         }
         E += sv;
         const int rmax_si = p.rmax[si];   // consumed after the update: its latency hides there
@@ -844,12 +1024,12 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
         ring_s[pos] = si;
         if (tabu > 0) {
             // tabu window (R-11): si enters, the (tabu+1)-th most recent flip leaves
-            if (owns(si)) { tcnt[si]++; tm |= ONE << lbit(si); }
+            if (owns(si)) { tcnt[lidx(si)]++; tm |= ONE << lbit(si); }
             const int r = ring_s[(pos + tabu) & (TABU_RING - 1)];
-            if (r >= 0 && owns(r) && --tcnt[r] == 0) tm &= ~(ONE << lbit(r));
+            if (r >= 0 && owns(r) && --tcnt[lidx(r)] == 0) tm &= ~(ONE << lbit(r));
         }
         if constexpr (TRACE) {
-            if (t == 0 && s == p.trace_slot && flips < p.tr_cap) {
+            if (tq == 0 && s == p.trace_slot && flips < p.tr_cap) {
                 p.tr_bit[flips] = si;
                 p.tr_E[flips] = E;
                 p.tr_phase[flips] = (int8_t)(phase == 2 ? 2 + min(round, 100) : phase);
@@ -913,20 +1093,21 @@ __global__ void __launch_bounds__(NTT) batch_kernel(const BatchParams p)
         const bits_t bb = xb ^ bdiff;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            const int ch = (c << lgNT) + t;
+            const int ch = (c << lgNTG) + tq;
             Xb[ch] = (uint8_t)(xb >> (8 * c));
             Bb[ch] = (uint8_t)(bb >> (8 * c));
             reinterpret_cast<int4*>(dp + ch * 8)[0] = make_int4(d[8 * c], d[8 * c + 1], d[8 * c + 2], d[8 * c + 3]);
             reinterpret_cast<int4*>(dp + ch * 8)[1] = make_int4(d[8 * c + 4], d[8 * c + 5], d[8 * c + 6], d[8 * c + 7]);
         }
-        if (t < TABU_RING) p.ring[(size_t)s * TABU_RING + t] = ring_s[(pos + t) & (TABU_RING - 1)];
-        if (t == 0) {
+        if (tq < TABU_RING) p.ring[(size_t)s * TABU_RING + t] = ring_s[(pos + t) & (TABU_RING - 1)];
+        if (tq == 0) {
             p.E[s] = E;
             p.ebest[s] = ebest;
             p.flips[s] = flips;
             atomicAdd(p.flip_total, (unsigned long long)flips);
         }
     }
+    if constexpr (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still write to it
 }
 
 }  // namespace dabs

@@ -5,7 +5,9 @@
 // and the exchange buffers.  A generation is GA seed -> batch -> merge ->
 // pack -> (exchange) -> import, all on one stream (R-25, R-26).
 // Citations: P:n = PAPER.md line n; R-x = DESIGN.md readings.
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
@@ -47,6 +49,7 @@ struct dabs_ctx {
     bool own_stream = false;
     // problem and tiling
     int n = 0, n_pad = 0, nwp = 0, C = 0, NT = 0;
+    int CL = 1;              // CTAs per search (2 = cluster tier)
     bool mw = false;
     int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
     GaConst ga{};
@@ -151,27 +154,37 @@ static int flip_factor(uint32_t milli, int n)
 // ---------------------------------------------------------------- kernels by tier
 using BatchFn = void (*)(const BatchParams);
 
-static BatchFn pick_batch(int C, int NT, bool trace)
+static BatchFn pick_batch(int C, int NT, int CL, bool trace)
 {
+    if (CL == 2) {
+        switch (NT) {
+        case 64: return trace ? batch_kernel<8, 64, 2, true> : batch_kernel<8, 64, 2, false>;
+        case 128: return trace ? batch_kernel<8, 128, 2, true> : batch_kernel<8, 128, 2, false>;
+        case 256: return trace ? batch_kernel<8, 256, 2, true> : batch_kernel<8, 256, 2, false>;
+        default: return trace ? batch_kernel<8, 512, 2, true> : batch_kernel<8, 512, 2, false>;
+        }
+    }
     if (NT > 32) {
         switch (NT) {
-        case 64: return trace ? batch_kernel<8, 64, true> : batch_kernel<8, 64, false>;
-        case 128: return trace ? batch_kernel<8, 128, true> : batch_kernel<8, 128, false>;
-        case 256: return trace ? batch_kernel<8, 256, true> : batch_kernel<8, 256, false>;
-        default: return trace ? batch_kernel<8, 512, true> : batch_kernel<8, 512, false>;
+        case 64: return trace ? batch_kernel<8, 64, 1, true> : batch_kernel<8, 64, 1, false>;
+        case 128: return trace ? batch_kernel<8, 128, 1, true> : batch_kernel<8, 128, 1, false>;
+        case 256: return trace ? batch_kernel<8, 256, 1, true> : batch_kernel<8, 256, 1, false>;
+        default: return trace ? batch_kernel<8, 512, 1, true> : batch_kernel<8, 512, 1, false>;
         }
     }
     switch (C) {
-    case 1: return trace ? batch_kernel<1, 32, true> : batch_kernel<1, 32, false>;
-    case 2: return trace ? batch_kernel<2, 32, true> : batch_kernel<2, 32, false>;
-    case 4: return trace ? batch_kernel<4, 32, true> : batch_kernel<4, 32, false>;
-    default: return trace ? batch_kernel<8, 32, true> : batch_kernel<8, 32, false>;
+    case 1: return trace ? batch_kernel<1, 32, 1, true> : batch_kernel<1, 32, 1, false>;
+    case 2: return trace ? batch_kernel<2, 32, 1, true> : batch_kernel<2, 32, 1, false>;
+    case 4: return trace ? batch_kernel<4, 32, 1, true> : batch_kernel<4, 32, 1, false>;
+    default: return trace ? batch_kernel<8, 32, 1, true> : batch_kernel<8, 32, 1, false>;
     }
 }
+static BatchFn pick_batch(const dabs_ctx* c, bool trace) { return pick_batch(c->C, c->NT, c->CL, trace); }
 
-static size_t row_smem(const dabs_ctx* c)   // one W row + tabu counts (+ sigma bytes, CTA tier)
+// per CTA: its part of one W row + tabu counts (+ sigma bytes, CTA tiers)
+static size_t row_smem(const dabs_ctx* c)
 {
-    return (size_t)(c->mw ? 4 : 3) * c->n_pad;
+    return (size_t)(c->mw ? 4 : 3) * (c->n_pad / c->CL);
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
@@ -201,7 +214,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
 {
     if (!out) return fail(DABS_E_ARG, "out is NULL");
     *out = nullptr;
-    if (n < 1 || n > 32768) return fail(DABS_E_ARG, "n=%d outside [1, 32768]", n);
+    if (n < 1 || n > 65536) return fail(DABS_E_ARG, "n=%d outside [1, 65536]", n);
     dabs_config cfg;
     dabs_config_default(&cfg);
     if (cfg_in) {
@@ -261,16 +274,21 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         while (C * 256 < n) C <<= 1;
         c->C = C;
     } else {
+        // one CTA of NT threads x 64 elements (n <= 32768), else a cluster of
+        // two such CTAs (n <= 65536).  DABS_CLUSTER=1 forces the
+        // cluster tier for every n > 4096 (A/B measurements).
         c->mw = true;
         c->C = 8;
+        const char* ev = getenv("DABS_CLUSTER");
+        c->CL = (n > 32768 || (ev && ev[0] == '1' && n > 4096)) ? 2 : 1;
         int NT = 64;
-        while (NT * 64 < n) NT <<= 1;
+        while (NT * 64 * c->CL < n) NT <<= 1;
         c->NT = NT;
     }
-    c->n_pad = c->NT * c->C * 8;
+    c->n_pad = c->NT * c->CL * c->C * 8;
     c->nwp = c->n_pad / 32;
     for (int tr = 0; tr < 2; tr++) {
-        cudaError_t e = cudaFuncSetAttribute(pick_batch(c->C, c->NT, tr != 0),
+        cudaError_t e = cudaFuncSetAttribute(pick_batch(c, tr != 0),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
@@ -283,9 +301,9 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         c->S = (int)cfg.slots_per_pool;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c->C, c->NT, false), c->NT, row_smem(c));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
-        const int conc = prop.multiProcessorCount * occ;
+        const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
         c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
                                                 // (TwoNeighbor runs 2n-1 main flips), more
                                                 // waves let the block scheduler balance them
@@ -449,7 +467,7 @@ extern "C" dabs_status dabs_create_csr(int32_t n, const int32_t* row_ptr, const 
     if (!out) return fail(DABS_E_ARG, "out is NULL");
     *out = nullptr;
     if (!row_ptr || !diag) return fail(DABS_E_ARG, "row_ptr / diag is NULL");
-    if (n < 1 || n > 32768) return fail(DABS_E_ARG, "n=%d outside [1, 32768]", n);
+    if (n < 1 || n > 65536) return fail(DABS_E_ARG, "n=%d outside [1, 65536]", n);
     if (row_ptr[0] != 0) return fail(DABS_E_ARG, "row_ptr[0] != 0");
     const int64_t nnz = row_ptr[n];
     if (nnz < 0 || nnz > (int64_t)n * (n - 1) / 2) return fail(DABS_E_ARG, "bad nnz %lld", (long long)nnz);
@@ -552,8 +570,24 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
 {
     BatchParams p = batch_params(c, seed, gen, slot0);
     p.order = order;
-    BatchFn fn = pick_batch(c->C, c->NT, trace);
-    fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
+    BatchFn fn = pick_batch(c, trace);
+    if (c->CL == 1) {
+        fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
+    } else {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(count * c->CL));
+        lc.blockDim = dim3((unsigned)c->NT);
+        lc.dynamicSmemBytes = row_smem(c);
+        lc.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c->CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&lc, fn, p));
+    }
     CK(cudaGetLastError());
     return DABS_OK;
 }
@@ -699,7 +733,7 @@ extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
                 o->dispatch[a][g] += d[(p * N_ALG + a) * N_GEN + g];
                 o->inserted[a][g] += in[(p * N_ALG + a) * N_GEN + g];
             }
-    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = c->NT; o->slots = c->slots; o->pools = c->P;
+    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = c->NT * c->CL; o->slots = c->slots; o->pools = c->P;
     o->T = c->T; o->B = c->B; o->cap = c->cap;
     return DABS_OK;
 }

@@ -84,6 +84,49 @@ def test_batch_parity(orc, lib, n):
     solver.close()
 
 
+@pytest.fixture
+def cluster_tier(monkeypatch):
+    """Force the 2-CTA cluster tier for every n > 4096."""
+    monkeypatch.setenv("DABS_CLUSTER", "1")
+
+
+@pytest.mark.parametrize("n", [4097, 5000, 9000, 20000, 32768])
+def test_batch_parity_cluster_forced(orc, lib, cluster_tier, n):
+    """The cluster tier (two CTAs per search, DSMEM swaps) at sizes the
+    single-CTA tier also covers: same bit-exact bar."""
+    from paper_2207_03069_b200 import workloads as wl
+    rng = np.random.default_rng(2000 + n)
+    U = wl.random_dense(n, seed=n, lo=-3000, hi=3000)
+    solver = lib.Solver(U, s_milli=150, b_milli=1500, pools=1, slots=2)
+    assert solver.stats().threads_per_search >= 128
+    for algo in ALGS:
+        st = random_state(orc, rng, U, n_ring=5)
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        compare_batch(orc, solver, U, st, D, algo, int(rng.integers(0, 2**63)), gslot=1,
+                      gen=int(rng.integers(0, 1000)), T=solver.T, B=solver.B, tabu=8)
+    solver.close()
+
+
+@pytest.mark.parametrize("n", [32769, 40000, 65536])
+def test_batch_parity_large_n(orc, lib, n):
+    """n > 32768 always runs on the cluster tier.  Short batches (s = b =
+    0.001, D = X with 40 bits changed) keep the oracle at a few seconds."""
+    from paper_2207_03069_b200 import workloads as wl
+    rng = np.random.default_rng(3000 + n)
+    U = wl.random_dense(n, seed=n, lo=-3000, hi=3000)
+    solver = lib.Solver(U, s_milli=1, b_milli=1, pools=1, slots=1)
+    assert solver.stats().threads_per_search == 1024
+    st0 = random_state(orc, rng, U, n_ring=3)
+    for algo in ALGS:
+        st = st0.copy()
+        D = st.x.copy()
+        D[rng.choice(n, 40, replace=False)] ^= 1
+        compare_batch(orc, solver, U, st, D, algo, int(rng.integers(0, 2**63)), gslot=0, gen=algo,
+                      T=solver.T, B=solver.B, tabu=8)
+        st0 = st                                # continue from a local minimum: shorter Greedy
+    solver.close()
+
+
 @pytest.mark.parametrize("n", [16, 200])
 def test_batch_parity_structured(orc, lib, n):
     """MaxCut-shaped (+-1, many ties) and zero-plateau instances stress the
@@ -187,6 +230,23 @@ def test_generation_parity(orc, lib, n, P, S, gens):
             reco["algo"], reco["genop"], reco["gen"], reco["slot"])
 
 
+def test_generation_parity_cluster(orc, lib, cluster_tier):
+    """Whole generations (GA, batches, merge) on the cluster tier."""
+    n, P, S = 5000, 2, 3
+    rng = np.random.default_rng(n)
+    U = rand_upper(rng, n, -200, 200)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=S, cap=20)
+    sysm = orc.System(U, cfg, world=1)
+    solver = lib.Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=20)
+    sysm.reset(9)
+    solver.reset(9)
+    for g in range(2):
+        sysm.generation()
+        solver.generation()
+        compare_world(orc, solver, sysm.ranks[0], P, g + 1)
+    assert solver.stats().total_flips == sysm.ranks[0].total_flips
+
+
 def test_k16_run_parity_and_optimum(orc, lib):
     """Config K16: single search; GPU run == oracle run, and it reaches the
     brute-force optimum over all 65536 vectors."""
@@ -254,6 +314,26 @@ def test_r32k_sampled_parity(orc, lib):
     np.testing.assert_array_equal(st.x, post["x"])
     np.testing.assert_array_equal(st.delta, post["delta"])
     # property at any size: E(BEST) equals Eq.(2) evaluated directly on the device
+    assert solver.energy(pk["best"]) == pk["ebest"]
+
+
+def test_r64k_sampled_parity(orc, lib):
+    """n = 65536 (the boundary's maximum, cluster tier; 8 GiB W) in the bench
+    launch configuration: one sampled slot recomputed by the oracle."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("R64K", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1)
+    solver.reset(4)
+    s = solver.slots - 1
+    pre = solver.read_slot(s)
+    solver.generation()
+    pk = solver.read_packet(s)
+    post = solver.read_slot(s)
+    st = orc.SlotState(pre["x"].copy(), pre["delta"].copy(), pre["E"], pre["ring"].copy())
+    ref = orc.batch(U, st, pk["D"], pk["algo"], T=solver.T, B=solver.B, tabu=8, seed=4, slot=s, gen=0)
+    assert ref.flips == pk["flips"] and ref.ebest == pk["ebest"]
+    np.testing.assert_array_equal(ref.best, pk["best"])
+    np.testing.assert_array_equal(st.delta, post["delta"])
     assert solver.energy(pk["best"]) == pk["ebest"]
 
 
