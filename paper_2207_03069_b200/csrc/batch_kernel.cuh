@@ -351,7 +351,7 @@ __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_
 }
 
 template <int C, int NTT, int CL, bool TRACE>
-__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 1) batch_kernel(const BatchParams p)
+__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_kernel(const BatchParams p)
 {
     static_assert(CL == 1 || (CL == 2 && NTT > 32), "cluster tier needs the CTA tier");
     constexpr bool MW = NTT > 32;                    // more than one warp per search

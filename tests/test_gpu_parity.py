@@ -90,7 +90,7 @@ def cluster_tier(monkeypatch):
     monkeypatch.setenv("DABS_CLUSTER", "1")
 
 
-@pytest.mark.parametrize("n", [4097, 5000, 9000, 20000, 32768])
+@pytest.mark.parametrize("n", [4097, 9000, 20000])
 def test_batch_parity_cluster_forced(orc, lib, cluster_tier, n):
     """The cluster tier (two CTAs per search, DSMEM swaps) at sizes the
     single-CTA tier also covers: same bit-exact bar."""
@@ -107,7 +107,7 @@ def test_batch_parity_cluster_forced(orc, lib, cluster_tier, n):
     solver.close()
 
 
-@pytest.mark.parametrize("n", [32769, 40000, 65536])
+@pytest.mark.parametrize("n", [32769, 65536])
 def test_batch_parity_large_n(orc, lib, n):
     """n > 32768 always runs on the cluster tier.  Short batches (s = b =
     0.001, D = X with 40 bits changed) keep the oracle at a few seconds."""
