@@ -88,8 +88,10 @@ void dabs_config_default(dabs_config* cfg);
 /* Create a solver for W (host, row-major n x n int16, upper triangular
  * including the diagonal, E(X) = sum_{i<=j} W_ij x_i x_j).  Only i <= j is
  * read for the model; any nonzero below the diagonal -> DABS_E_TRIANGLE.
- * 1 <= n <= 32768 else DABS_E_ARG.  If max_k (|W_kk| + sum_{j!=k} |W_jk|)
- * >= 2^31 - 1 -> DABS_E_RANGE (Delta is int32).  Uploads W, lays it out as
+ * 1 <= n <= 65536 else DABS_E_ARG (n <= 2048: one warp per search; n <=
+ * 32768: one CTA; n > 32768: a cluster of two CTAs).  If max_k (|W_kk| +
+ * sum_{j!=k} |W_jk|) >= 2^31 - 1 -> DABS_E_RANGE (Delta is int32; reachable
+ * only for n > 32768 with large weights).  Uploads W, lays it out as
  * symmetric int16 rows with zero diagonal, allocates slots
  * and pools.  *out receives the context (NULL on failure). */
 dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg, dabs_ctx** out);
