@@ -67,7 +67,10 @@ typedef struct {
     uint32_t tabu_period;     /* P:487-489; default 8; <= 31 */
     uint32_t pool_capacity;   /* P:703; default 100 */
     uint32_t eps_ppm;         /* exploration probability; default 50000 = 5% */
-    uint32_t genop_mask;      /* enabled genetic operations, bit g (P:174 order); default 0xFF */
+    uint32_t genop_mask;      /* enabled genetic operations, bit g (P:174 order); default 0xFF.
+                                 Bit 8 = mutation after crossover, the ABS solver's only
+                                 operation (R-27): genop_mask = 0x100 with
+                                 algo_mask = 0x2 (CyclicMin) is the ABS ablation mode */
     uint32_t algo_mask;       /* enabled main algorithms, bit a (P:169 order); default 0x1F */
     uint32_t pools_per_gpu;   /* solution pools on this rank; default 1 */
     uint32_t slots_per_pool;  /* concurrent searches per pool; 0 = auto (fill the GPU) */
@@ -80,6 +83,10 @@ typedef struct {
     dabs_alloc_fn alloc;      /* NULL = cudaMalloc */
     dabs_free_fn free;
     void* user;               /* passed to the hooks */
+    uint32_t restart_gens;    /* restart-on-merge (R-28): after this many
+                                 generations without a box-wide improvement, pools and
+                                 slots start afresh (the best is kept); 0 = off (default) */
+    uint32_t reserved;
 } dabs_config;
 
 /* Fills the defaults listed above. */
@@ -91,7 +98,7 @@ void dabs_config_default(dabs_config* cfg);
  * 1 <= n <= 65536 else DABS_E_ARG (n <= 2048: one warp per search; n <=
  * 32768: one CTA; n > 32768: a cluster of two CTAs).  If max_k (|W_kk| +
  * sum_{j!=k} |W_jk|) >= 2^31 - 1 -> DABS_E_RANGE (Delta is int32; reachable
- * only for n > 32768 with large weights).  Uploads W, lays it out as
+ * only at n = 65536 with weights of -32768).  Uploads W, lays it out as
  * symmetric int16 rows with zero diagonal, allocates slots
  * and pools.  *out receives the context (NULL on failure). */
 dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg, dabs_ctx** out);
@@ -140,8 +147,9 @@ typedef struct {
     int64_t best_energy;
     int32_t best_algo, best_genop;   /* first-best record */
     int32_t best_generation, best_slot;
-    uint64_t dispatch[5][8];     /* [algorithm][genop] packets issued (Table V) */
-    uint64_t inserted[5][8];     /* [algorithm][genop] results that entered a pool */
+    uint64_t dispatch[5][9];     /* [algorithm][genop] packets issued (Table V) */
+    uint64_t inserted[5][9];     /* [algorithm][genop] results that entered a pool */
+    uint64_t restarts;           /* restart-on-merge events since reset */
     int32_t n, n_pad, threads_per_search, slots, pools, T, B;
     int32_t cap;
 } dabs_stats;
@@ -170,8 +178,8 @@ dabs_status dabs_read_pool(const dabs_ctx* ctx, uint32_t pool, uint8_t* X /* cap
                            int64_t* E, uint64_t* seq, uint8_t* algo, uint8_t* genop);
 dabs_status dabs_read_packet(const dabs_ctx* ctx, uint32_t slot, uint8_t* D, int32_t* algo,
                              int32_t* genop, uint8_t* best, int64_t* ebest, int64_t* flips);
-dabs_status dabs_read_stats_pool(const dabs_ctx* ctx, uint32_t pool, uint64_t* dispatch /*5*8*/,
-                                 uint64_t* inserted /*5*8*/);
+dabs_status dabs_read_stats_pool(const dabs_ctx* ctx, uint32_t pool, uint64_t* dispatch /*5*9*/,
+                                 uint64_t* inserted /*5*9*/);
 
 /* Enable per-flip tracing of one local slot in production generations
  * (trace_cap flips per batch; -1 slot disables).  Read after a generation. */

@@ -32,9 +32,10 @@ typedef unsigned __int128 u128;
 /* main search algorithms, in the paper's order */
 enum { ALG_MAXMIN = 0, ALG_CYCLICMIN = 1, ALG_RANDOMMIN = 2, ALG_POSITIVEMIN = 3,
        ALG_TWONEIGHBOR = 4, N_ALG = 5 };
-/* genetic operations, in the paper's order */
+/* genetic operations, in the paper's order, then the ABS solver's
+   single operation "mutation after crossover" (ablation mode, R-27) */
 enum { GEN_MUTATION = 0, GEN_CROSSOVER = 1, GEN_XROSSOVER = 2, GEN_ZERO = 3, GEN_ONE = 4,
-       GEN_INTERVALZERO = 5, GEN_BEST = 6, GEN_RANDOM = 7, N_GEN = 8 };
+       GEN_INTERVALZERO = 5, GEN_BEST = 6, GEN_RANDOM = 7, GEN_MUTCROSS = 8, N_GEN = 9 };
 /* phases recorded in the trace: 0 Straight, 1 Greedy, 2+r main round r */
 enum { PH_STRAIGHT = 0, PH_GREEDY = 1, PH_MAIN = 2 };
 /* Philox purposes (R-16) */
@@ -524,8 +525,11 @@ typedef struct {
     uint8_t* D; uint8_t* palgo; uint8_t* pgenop;
     uint8_t* rbest; int64_t* rE; int64_t* rflips;
     /* statistics */
-    uint64_t* dispatch;   /* P * 5 * 8 */
-    uint64_t* inserted;   /* P * 5 * 8 */
+    uint64_t* dispatch;   /* P * N_ALG * N_GEN */
+    uint64_t* inserted;   /* P * N_ALG * N_GEN */
+    /* restart-on-merge (R-28): generations without a box-wide
+       improvement, the limit (0 = off), restarts so far */
+    uint32_t stall, restart_gens, restarts;
     /* run-level */
     int64_t best_E; uint8_t* best_X; int best_algo, best_genop; int64_t best_gen; int64_t best_slot;
     uint64_t total_flips;
@@ -545,18 +549,19 @@ static void pool_alloc(pool_t* p, int cap, int n)
 static void pool_free(pool_t* p) { free(p->X); free(p->E); free(p->seq); free(p->algo); free(p->genop); }
 
 /* a pool starts as random vectors with +inf energy and random
-   algorithm / genop columns (R-19). */
-static void pool_init(const world_t* w, pool_t* p, uint32_t gpool)
+   algorithm / genop columns (R-19).  `gen` = 0 at reset, the generation
+   counter at a restart (R-28). */
+static void pool_init(const world_t* w, pool_t* p, uint32_t gpool, uint32_t gen)
 {
     int n = w->n;
     for (int r = 0; r < w->cap; r++) {
         for (int k = 0; k < n; k++) {
             uint32_t o[4];
-            rng4(w->seed, PUR_POOL_INIT, (uint32_t)(k / 32), gpool, 0, (uint32_t)r, o);
+            rng4(w->seed, PUR_POOL_INIT, (uint32_t)(k / 32), gpool, gen, (uint32_t)r, o);
             p->X[(size_t)r * n + k] = (uint8_t)((o[0] >> (k % 32)) & 1u);
         }
         uint32_t o[4];
-        rng4(w->seed, PUR_POOL_TAGS, 0, gpool, 0, (uint32_t)r, o);
+        rng4(w->seed, PUR_POOL_TAGS, 0, gpool, gen, (uint32_t)r, o);
         p->genop[r] = (uint8_t)w->gens[pick(o[0], (uint32_t)w->n_gen)];
         p->algo[r] = (uint8_t)w->algs[pick(o[1], (uint32_t)w->n_alg)];
         p->E[r] = ORC_E_INF;
@@ -611,24 +616,35 @@ void orc_world_free(void* vw)
 }
 
 void orc_world_set_checked(void* vw, int checked) { ((world_t*)vw)->checked = checked; }
+void orc_world_set_restart(void* vw, uint32_t gens) { ((world_t*)vw)->restart_gens = gens; }
+uint32_t orc_world_restarts(void* vw) { return ((world_t*)vw)->restarts; }
 
-/* Reset: pools from Philox, slots at X=0, E=0, Delta_k=W_kk (P:331-332,
-   P:518-519), empty tabu rings, counters zero, generation 0. */
-void orc_world_reset(void* vw, uint64_t seed)
+/* pools from Philox (counter generation `gen`), slots at X=0, E=0,
+   Delta_k=W_kk, empty tabu rings */
+static void start_pools_and_slots(world_t* w, uint32_t gen)
 {
-    world_t* w = (world_t*)vw;
     int n = w->n, ns = w->P * w->S;
-    w->seed = seed;
-    w->gen = 0;
-    for (int p = 0; p < w->P; p++) pool_init(w, &w->pools[p], (uint32_t)(w->rank * w->P + p));
+    for (int p = 0; p < w->P; p++) pool_init(w, &w->pools[p], (uint32_t)(w->rank * w->P + p), gen);
     uint32_t succ = (uint32_t)(((w->rank + 1) * w->P) % (w->world * w->P));
-    pool_init(w, &w->nbr, succ);
+    pool_init(w, &w->nbr, succ, gen);
     memset(w->sx, 0, (size_t)ns * n);
     for (int s = 0; s < ns; s++) {
         for (int k = 0; k < n; k++) w->sdelta[(size_t)s * n + k] = Uij(w->U, n, k, k);
         w->sE[s] = 0;
         for (int j = 0; j < ORC_TABU_MAX; j++) w->sring[(size_t)s * ORC_TABU_MAX + j] = -1;
     }
+}
+
+/* Reset: pools and slots as above, counters zero, generation 0. */
+void orc_world_reset(void* vw, uint64_t seed)
+{
+    world_t* w = (world_t*)vw;
+    int n = w->n;
+    w->seed = seed;
+    w->gen = 0;
+    start_pools_and_slots(w, 0);
+    w->stall = 0;
+    w->restarts = 0;
     memset(w->dispatch, 0, sizeof(uint64_t) * w->P * N_ALG * N_GEN);
     memset(w->inserted, 0, sizeof(uint64_t) * w->P * N_ALG * N_GEN);
     w->best_E = ORC_E_INF; w->best_algo = -1; w->best_genop = -1; w->best_gen = -1; w->best_slot = -1;
@@ -659,6 +675,7 @@ void orc_build_target(int genop, const uint8_t* A, const uint8_t* Bp, const uint
         rng4(seed, PUR_GA_MASK, (uint32_t)(k / 32), gs, gen, 0, m);
         int bit = k % 32;
         int m0 = (m[0] >> bit) & 1, m1 = (m[1] >> bit) & 1, m2 = (m[2] >> bit) & 1;
+        int m3 = (m[3] >> bit) & 1;
         int p8 = m0 & m1 & m2;   /* probability 1/8 (R-20) */
         int v = 0;
         switch (genop) {
@@ -671,6 +688,7 @@ void orc_build_target(int genop, const uint8_t* A, const uint8_t* Bp, const uint
             v = ((uint32_t)((k - (int)start + n) % n) < L) ? 0 : A[k]; break;
         case GEN_BEST: v = best0[k]; break;                            /* P:595-596 */
         case GEN_RANDOM: v = m0; break;                                /* P:597-598 */
+        case GEN_MUTCROSS: v = (m3 ? A[k] : Bp[k]) ^ p8; break;        /* P:188-189, R-27 */
         }
         D[k] = (uint8_t)v;
     }
@@ -856,8 +874,20 @@ void orc_world_import(void* vw, const uint8_t* all)
         w->best_algo = ba; w->best_genop = bg;
         w->best_gen = (int64_t)(bs >> 32) - 1;
         w->best_slot = (int64_t)(bs & 0xFFFFFFFFu);
+        w->stall = 0;
+    } else {
+        w->stall++;
     }
     w->gen++;
+    /* restart-on-merge (R-28): after restart_gens generations
+       without a box-wide improvement, every rank re-initialises its pools and
+       slots (the decision uses only gathered data, so all ranks agree); the
+       run's best is kept */
+    if (w->restart_gens && w->stall >= w->restart_gens) {
+        start_pools_and_slots(w, w->gen);
+        w->stall = 0;
+        w->restarts++;
+    }
 }
 
 /* ---- accessors for the Python wrapper ---- */

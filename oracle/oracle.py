@@ -23,9 +23,9 @@ SRC = os.path.join(HERE, "dabs_oracle.c")
 LIB = os.path.join(HERE, "libdabs_oracle.so")
 
 TABU_MAX = 32
-N_ALG, N_GEN = 5, 8
+N_ALG, N_GEN = 5, 9   # 8 paper genops + ABS's mutation-after-crossover (R-27)
 ALG_NAMES = ["MaxMin", "CyclicMin", "RandomMin", "PositiveMin", "TwoNeighbor"]
-GEN_NAMES = ["Mutation", "Crossover", "Xrossover", "Zero", "One", "IntervalZero", "Best", "Random"]
+GEN_NAMES = ["Mutation", "Crossover", "Xrossover", "Zero", "One", "IntervalZero", "Best", "Random", "MutCross"]
 E_INF = np.iinfo(np.int64).max
 
 
@@ -66,6 +66,9 @@ def lib():
         L.orc_world_new.restype = P
         L.orc_world_free.argtypes = [P]
         L.orc_world_set_checked.argtypes = [P, C.c_int]
+        L.orc_world_set_restart.argtypes = [P, u32]
+        L.orc_world_restarts.argtypes = [P]
+        L.orc_world_restarts.restype = u32
         L.orc_world_reset.argtypes = [P, u64]
         L.orc_world_generation_local.argtypes = [P]
         L.orc_world_generation_local.restype = C.c_int
@@ -251,6 +254,7 @@ class Config:
     algo_mask: int = 0x1F
     pools: int = 1          # pools per rank
     slots: int = 1          # slots per pool
+    restart_gens: int = 0   # restart-on-merge after this many stalled generations (R-28); 0 = off
 
 
 class World:
@@ -266,6 +270,7 @@ class World:
                                  cfg.eps_ppm, cfg.genop_mask, cfg.algo_mask,
                                  cfg.pools, cfg.slots, rank, world)
         L.orc_world_set_checked(self.h, int(checked))
+        L.orc_world_set_restart(self.h, int(cfg.restart_gens))
         self.payload_bytes = int(L.orc_world_payload_bytes(self.h))
 
     def __del__(self):
@@ -288,6 +293,10 @@ class World:
     @property
     def total_flips(self):
         return int(lib().orc_world_total_flips(self.h))
+
+    @property
+    def restarts(self):
+        return int(lib().orc_world_restarts(self.h))
 
     @property
     def gen_flips(self):

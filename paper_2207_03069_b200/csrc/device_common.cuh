@@ -7,9 +7,10 @@
 namespace dabs {
 
 constexpr int ALG_MAXMIN = 0, ALG_CYCLIC = 1, ALG_RANDOM = 2, ALG_POSMIN = 3, ALG_TWO = 4;
-constexpr int N_ALG = 5, N_GEN = 8;
+constexpr int N_ALG = 5, N_GEN = 9;
+// the paper's eight genops + the ABS solver's mutation after crossover (R-27)
 constexpr int GEN_MUTATION = 0, GEN_CROSSOVER = 1, GEN_XROSSOVER = 2, GEN_ZERO = 3, GEN_ONE = 4,
-              GEN_INTERVALZERO = 5, GEN_BEST = 6, GEN_RANDOM = 7;
+              GEN_INTERVALZERO = 5, GEN_BEST = 6, GEN_RANDOM = 7, GEN_MUTCROSS = 8;
 constexpr int TABU_RING = 32;   // ring slots kept per search (R-11); tabu period <= 31
 constexpr uint32_t PUR_POOL_INIT = 1, PUR_GA_CHOICE = 2, PUR_GA_PARENT = 3, PUR_GA_MASK = 4,
                    PUR_MAXMIN = 5, PUR_RANDMIN = 6, PUR_POSMIN = 7, PUR_POOL_TAGS = 8;

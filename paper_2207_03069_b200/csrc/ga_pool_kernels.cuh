@@ -124,28 +124,28 @@ struct GaConst {
     int n, nwp, cap, P, S;
     uint32_t eps_thr;
     int n_gen, n_alg;
-    int gens[8];
-    int algs[5];
+    int gens[N_GEN];
+    int algs[N_ALG];
     uint64_t seed;
 };
 
 // Pools start as random vectors with +inf energy and random tags (P:601-602,
 // R-19).  blockIdx.x = local pool p (p == P: the successor snapshot, global
 // id nbr_gid); blockIdx.y = row.
-__global__ void init_pools_kernel(GaConst g, PoolView* pools, uint32_t gid0, uint32_t nbr_gid)
+__global__ void init_pools_kernel(GaConst g, PoolView* pools, uint32_t gid0, uint32_t nbr_gid, uint32_t gen)
 {
     const int p = blockIdx.x, r = blockIdx.y;
     const uint32_t gp = (p < g.P) ? gid0 + (uint32_t)p : nbr_gid;
     PoolView pv = pools[p];
     const int full = g.n >> 5, rem = g.n & 31;
     for (int w = threadIdx.x; w < g.nwp; w += blockDim.x) {
-        uint32_t v = rng4(g.seed, PUR_POOL_INIT, (uint32_t)w, gp, 0, (uint32_t)r).x;
+        uint32_t v = rng4(g.seed, PUR_POOL_INIT, (uint32_t)w, gp, gen, (uint32_t)r).x;
         if (w > full || (w == full && rem == 0)) v = 0;
         else if (w == full) v &= (1u << rem) - 1u;
         pv.X[(size_t)r * g.nwp + w] = v;
     }
     if (threadIdx.x == 0) {
-        const uint4 o = rng4(g.seed, PUR_POOL_TAGS, 0, gp, 0, (uint32_t)r);
+        const uint4 o = rng4(g.seed, PUR_POOL_TAGS, 0, gp, gen, (uint32_t)r);
         pv.genop[r] = (uint8_t)g.gens[pick_u(o.x, (uint32_t)g.n_gen)];
         pv.algo[r] = (uint8_t)g.algs[pick_u(o.y, (uint32_t)g.n_alg)];
         pv.E[r] = E_INF;
@@ -209,6 +209,7 @@ __global__ void ga_seed_kernel(GaConst g, const PoolView* __restrict__ pools, ui
             break;
         }
         case GEN_BEST: v = pool.X[w]; break;
+        case GEN_MUTCROSS: v = ((A[w] & m.w) | (Bv[w] & ~m.w)) ^ p8; break;
         default: v = m.x; break;   // GEN_RANDOM
         }
         const int64_t rem = (int64_t)n - (int64_t)w * 32;   // clear bits >= n

@@ -89,6 +89,8 @@ struct dabs_ctx {
     uint64_t seed = 0;
     uint32_t gen = 0;
     uint64_t total_flips = 0, local_flips = 0;
+    uint32_t stall = 0;          // generations without a box-wide improvement (R-28)
+    uint64_t restarts = 0;
     int64_t best_E = E_INF;
     std::vector<uint8_t> best_X;
     int32_t rec[4] = {-1, -1, -1, -1};
@@ -224,7 +226,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     if (cfg.tabu_period > 31) return fail(DABS_E_ARG, "tabu_period > 31");
     if (cfg.pool_capacity < 1 || cfg.pool_capacity > 1024) return fail(DABS_E_ARG, "pool_capacity outside [1,1024]");
     if (cfg.s_milli < 1 || cfg.b_milli < 1) return fail(DABS_E_ARG, "s and b must be positive");
-    if ((cfg.genop_mask & 0xFF) == 0 || (cfg.algo_mask & 0x1F) == 0) return fail(DABS_E_ARG, "empty genop/algo mask");
+    if ((cfg.genop_mask & 0x1FF) == 0 || (cfg.algo_mask & 0x1F) == 0) return fail(DABS_E_ARG, "empty genop/algo mask");
     if (cfg.eps_ppm > 1000000) return fail(DABS_E_ARG, "eps_ppm > 1e6");
     if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return fail(DABS_E_ARG, "bad rank/world");
     if (cfg.world > 1 && !cfg.exchange) return fail(DABS_E_ARG, "world > 1 needs an exchange hook");
@@ -547,7 +549,9 @@ extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)
                                                        c->E, c->ring);
     const uint32_t gid0 = (uint32_t)(c->cfg.rank * c->P);
     const uint32_t nbr_gid = (uint32_t)(((c->cfg.rank + 1) * c->P) % (c->cfg.world * c->P));
-    init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, c->stream>>>(c->ga, c->pools_d, gid0, nbr_gid);
+    init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, c->stream>>>(c->ga, c->pools_d, gid0, nbr_gid, 0u);
+    c->stall = 0;
+    c->restarts = 0;
     CK(cudaMemsetAsync(c->dispatch, 0, 8 * c->P * N_ALG * N_GEN, c->stream));
     CK(cudaMemsetAsync(c->inserted, 0, 8 * c->P * N_ALG * N_GEN, c->stream));
     CK(cudaMemsetAsync(c->flip_total, 0, 8, c->stream));
@@ -661,8 +665,23 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
         c->rec[2] = (int32_t)((sums[br].bestSeq >> 32) - 1);
         c->rec[3] = (int32_t)(sums[br].bestSeq & 0xFFFFFFFFu);
         c->ttb_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - c->t_reset).count();
+        c->stall = 0;
+    } else {
+        c->stall++;
     }
     c->gen++;
+    // restart-on-merge (R-28): the decision uses gathered data only,
+    // so every rank restarts in the same generation; the run's best is kept
+    if (c->cfg.restart_gens && c->stall >= c->cfg.restart_gens) {
+        init_slots_kernel<<<c->slots, 256, 0, st>>>(c->slots, c->n_pad, c->nwp, c->diag, c->X, c->delta, c->E,
+                                                    c->ring);
+        const uint32_t gid0 = (uint32_t)(c->cfg.rank * c->P);
+        const uint32_t nbr_gid = (uint32_t)(((c->cfg.rank + 1) * c->P) % (c->cfg.world * c->P));
+        init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, st>>>(c->ga, c->pools_d, gid0, nbr_gid, c->gen);
+        CK(cudaGetLastError());
+        c->stall = 0;
+        c->restarts++;
+    }
     return DABS_OK;
 }
 
@@ -722,6 +741,7 @@ extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
     o->ga_ms_last = c->ga_ms;
     o->merge_ms_last = c->merge_ms;
     o->best_energy = c->best_E;
+    o->restarts = c->restarts;
     o->best_algo = c->rec[0]; o->best_genop = c->rec[1]; o->best_generation = c->rec[2]; o->best_slot = c->rec[3];
     std::vector<unsigned long long> d(c->P * N_ALG * N_GEN), in(c->P * N_ALG * N_GEN);
     if (cudaMemcpy(d.data(), c->dispatch, 8 * d.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||

@@ -34,7 +34,7 @@ class dabs_config(C.Structure):
         ("slots_per_pool", C.c_uint32), ("target_energy", C.c_int64), ("time_limit_ns", C.c_uint64),
         ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
         ("cuda_stream", C.c_void_p), ("exchange", EXCHANGE_FN), ("alloc", ALLOC_FN), ("free", FREE_FN),
-        ("user", C.c_void_p),
+        ("user", C.c_void_p), ("restart_gens", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 
@@ -46,7 +46,7 @@ class dabs_stats(C.Structure):
         ("best_energy", C.c_int64),
         ("best_algo", C.c_int32), ("best_genop", C.c_int32), ("best_generation", C.c_int32),
         ("best_slot", C.c_int32),
-        ("dispatch", (C.c_uint64 * 8) * 5), ("inserted", (C.c_uint64 * 8) * 5),
+        ("dispatch", (C.c_uint64 * 9) * 5), ("inserted", (C.c_uint64 * 9) * 5), ("restarts", C.c_uint64),
         ("n", C.c_int32), ("n_pad", C.c_int32), ("threads_per_search", C.c_int32), ("slots", C.c_int32),
         ("pools", C.c_int32), ("T", C.c_int32), ("B", C.c_int32), ("cap", C.c_int32),
     ]
@@ -137,6 +137,7 @@ class Solver:
 
     def __init__(self, W: np.ndarray | None, *, csr=None, s_milli: int = 100, b_milli: int = 1000,
                  tabu: int = 8, cap: int = 100, eps_ppm: int = 50000, genop_mask: int = 0xFF, algo_mask: int = 0x1F,
+                 restart_gens: int = 0,
                  pools: int = 1, slots: int = 0, target: int | None = None, time_limit_ns: int = 0,
                  rank: int = 0, world: int = 1, device: int = -1, stream=None, exchange=None):
         L = load()
@@ -156,6 +157,7 @@ class Solver:
         cfg.s_milli, cfg.b_milli, cfg.tabu_period, cfg.pool_capacity = s_milli, b_milli, tabu, cap
         cfg.eps_ppm, cfg.genop_mask, cfg.algo_mask = eps_ppm, genop_mask, algo_mask
         cfg.pools_per_gpu, cfg.slots_per_pool = pools, slots
+        cfg.restart_gens = restart_gens
         cfg.target_energy = INT64_MIN if target is None else int(target)
         cfg.time_limit_ns = time_limit_ns
         cfg.rank, cfg.world, cfg.device = rank, world, device
@@ -285,8 +287,8 @@ class Solver:
         return dict(D=D, algo=int(a[0]), genop=int(g[0]), best=best, ebest=int(eb[0]), flips=int(fl[0]))
 
     def read_stats_pool(self, pool: int):
-        d = np.zeros((5, 8), np.uint64)
-        i = np.zeros((5, 8), np.uint64)
+        d = np.zeros((5, 9), np.uint64)
+        i = np.zeros((5, 9), np.uint64)
         _check(load().dabs_read_stats_pool(self.h, pool, _p(d), _p(i)))
         return d, i
 

@@ -204,8 +204,8 @@ def make(config: str, seed: int = 1):
         return random_dense(32768, seed), dict(s_milli=100, b_milli=1000)
     if config == "R64K":
         # the largest n the boundary accepts (cluster tier);
-        # |U| <= 16383 keeps max_k sum_j |W_kj| < 2^31 (dabs_create's range check)
-        return random_dense(65536, seed, -16383, 16383), dict(s_milli=100, b_milli=1000)
+        # |U| <= 32767 keeps max_k sum_j |W_kj| <= 65536 * 32767 < 2^31 - 1
+        return random_dense(65536, seed), dict(s_milli=100, b_milli=1000)
     if config.startswith("QASP"):               # QASP1 / QASP16 / QASP256 (resolution r)
         r = int(config[4:] or 1)
         U, off, _, _, _ = qasp_like(5627, 40279, r, seed)

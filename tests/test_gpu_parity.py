@@ -179,17 +179,18 @@ def test_create_errors(lib):
         lib.Solver(np.zeros((0, 0), np.int16))
     with pytest.raises(lib.DabsError, match="E_ARG"):
         lib.Solver(np.zeros((4, 4), np.int16), tabu=40)
-    # int16 weights with n <= 32768 can never overflow int32 Delta
-    # (32768 * 32767 < 2^31 - 1); at n = 65536 they can (checked via CSR)
+    # |Delta_k| <= |W_kk| + sum_j |W_kj| <= n * 32768: only n = 65536 with
+    # -32768 weights reaches 2^31 (checked via CSR: one full row)
     n = 65536
     rp = np.zeros(n + 1, np.int32)
     rp[1:] = n - 1
     col = np.arange(1, n, dtype=np.int32)
-    val = np.full(n - 1, 32767, np.int16)
+    val = np.full(n - 1, -32768, np.int16)
     diag = np.zeros(n, np.int16)
+    diag[0] = -32768
     with pytest.raises(lib.DabsError, match="E_RANGE"):
         lib.Solver(None, csr=(rp, col, val, diag))
-    val[:] = 16383                              # max row sum 65535 * 16383 < 2^31 - 1: accepted
+    val[:] = 32767                              # 32768 + 65535 * 32767 < 2^31 - 1: accepted
     lib.Solver(None, csr=(rp, col, val, diag), pools=1, slots=1).close()
     rp2 = np.zeros(n + 2, np.int32)
     with pytest.raises(lib.DabsError, match="E_ARG"):
@@ -248,6 +249,29 @@ def test_generation_parity(orc, lib, n, P, S, gens):
         assert st.total_flips == sysm.ranks[0].total_flips
         assert (st.best_algo, st.best_genop, st.best_generation, st.best_slot) == (
             reco["algo"], reco["genop"], reco["gen"], reco["slot"])
+
+
+@pytest.mark.parametrize("variant", ["abs", "restart"])
+def test_generation_parity_variants(orc, lib, variant):
+    """SURVEY f4 variants: the ABS ablation mode (CyclicMin only + mutation
+    after crossover, R-27) and restart-on-merge (R-28), whole generations."""
+    n, P, S = 60, 2, 3
+    rng = np.random.default_rng(77)
+    U = rand_upper(rng, n, -20, 20)
+    kw = dict(genop_mask=1 << 8, algo_mask=1 << 1) if variant == "abs" else dict(restart_gens=2)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=S, cap=8, **kw)
+    sysm = orc.System(U, cfg, world=1)
+    solver = lib.Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=8, **kw)
+    sysm.reset(21)
+    solver.reset(21)
+    for g in range(25):
+        sysm.generation()
+        solver.generation()
+        compare_world(orc, solver, sysm.ranks[0], P, g + 1)
+        assert solver.stats().restarts == sysm.ranks[0].restarts
+        assert solver.best()[0] == sysm.ranks[0].best()[0]
+    if variant == "restart":
+        assert sysm.ranks[0].restarts >= 1
 
 
 def test_generation_parity_cluster(orc, lib, cluster_tier):

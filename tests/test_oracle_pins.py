@@ -425,6 +425,112 @@ def test_genops(orc):
     assert abs(rnd.mean() - 0.5) < 0.02
 
 
+def test_mutcross_genop(orc):
+    """R-27 (ABS): mutation after crossover.  With equal parents it
+    is exactly Mutation (same mask draws); its crossover part D xor (mutation
+    mask) takes every bit from A or B, about half from each, independently of
+    the mutation mask."""
+    rng = np.random.default_rng(9)
+    n = 20000
+    A = rng.integers(0, 2, n).astype(np.uint8)
+    Bv = rng.integers(0, 2, n).astype(np.uint8)
+    kw = dict(seed=11, gslot=3, gen=5)
+    mut_mask = orc.build_target(0, A, Bv, A, **kw) ^ A                  # Mutation's p8 mask
+    assert np.array_equal(orc.build_target(8, A, A, A, **kw), A ^ mut_mask)
+    D = orc.build_target(8, A, Bv, A, **kw)
+    cx = D ^ mut_mask
+    assert np.all((cx == A) | (cx == Bv))
+    diff = A != Bv
+    took_a = cx[diff] == A[diff]
+    assert abs(took_a.mean() - 0.5) < 0.02
+    m = mut_mask[diff].astype(bool)                                     # independence of the two masks
+    assert abs(took_a[m].mean() - took_a[~m].mean()) < 0.05
+    # the crossover part is not Crossover's own mask (a fresh word, R-27)
+    assert not np.array_equal(cx, orc.build_target(1, A, Bv, A, **kw))
+
+
+def _improvements(sysm, gens):
+    out, prev = [], orc_E_inf()
+    w = sysm.ranks[0]
+    for _ in range(gens):
+        sysm.generation()
+        E = w.best()[0]
+        out.append(E < prev)
+        prev = min(prev, E)
+    return out
+
+
+def orc_E_inf():
+    return 2**63 - 1
+
+
+def test_restart_on_merge(orc):
+    """R-28: after R generations without a box-wide improvement,
+    pools become fresh sentinel pools and slots start again at X = 0; the run
+    is identical to the run without restarts up to that point, the best never
+    gets worse, and every rank restarts in the same generation."""
+    rng = np.random.default_rng(5)
+    n = 24
+    U = rand_upper(rng, n, -20, 20)
+    base = orc.Config(s_milli=100, b_milli=1000, pools=2, slots=3, cap=8)
+    ref = orc.System(U, base, world=2)
+    ref.reset(3)
+    imp = _improvements(ref, 30)
+    R = 3
+    # first generation index g (0-based) ending an R-long stall
+    stall, first = 0, None
+    for g, i in enumerate(imp):
+        stall = 0 if i else stall + 1
+        if stall >= R:
+            first = g
+            break
+    assert first is not None, "instance must stall"
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=2, slots=3, cap=8, restart_gens=R)
+    sysm = orc.System(U, cfg, world=2)
+    sysm.reset(3)
+    a = orc.System(U, base, world=2)
+    a.reset(3)
+    for g in range(first + 1):
+        sysm.generation()
+        a.generation()
+        want = 1 if g == first else 0
+        for w in sysm.ranks:
+            assert w.restarts == want
+        if g < first:
+            for p in range(2):
+                assert np.array_equal(sysm.ranks[0].pool(p)["X"], a.ranks[0].pool(p)["X"])
+    for w in sysm.ranks:
+        for p in range(cfg.pools):
+            assert (w.pool(p)["E"] == orc.E_INF).all()
+        for s_ in range(cfg.pools * cfg.slots):
+            st = w.slot(s_)
+            assert st.E == 0 and not st.x.any()
+            assert np.array_equal(st.delta, np.diag(U).astype(np.int32))
+    E_before = sysm.ranks[0].best()[0]
+    for _ in range(10):
+        sysm.generation()
+        assert sysm.ranks[0].best()[0] <= E_before
+    assert sysm.ranks[0].restarts == sysm.ranks[1].restarts >= 1
+
+
+def test_abs_mode_reaches_small_optimum(orc):
+    """ABS ablation mode (CyclicMin only + mutation after crossover) is a
+    working solver: it reaches brute-force optima of small instances."""
+    rng = np.random.default_rng(43)
+    hits = 0
+    for trial in range(10):
+        n = int(rng.integers(6, 15))
+        U = rand_upper(rng, n, -8, 8)
+        opt = bruteforce_min(U)
+        cfg = orc.Config(s_milli=100, b_milli=1000, pools=1, slots=4, genop_mask=1 << 8, algo_mask=1 << 1)
+        sysm = orc.System(U, cfg)
+        E, X, _ = sysm.run(seed=trial, flip_budget=200000, target=opt)
+        hits += int(E == opt)
+        d, _ = sysm.ranks[0].stats()
+        assert d.sum() == d[:, 1, 8].sum() > 0           # only (CyclicMin, MutCross) dispatched
+    assert hits >= 9
+
+
 def test_adaptive_choice_mixture(orc):
     """with probability eps a uniform genop / algorithm, else the tag
     of a uniform pool row.  Expected P(g) = (1-eps) frac_g + eps/8."""
