@@ -350,6 +350,17 @@ __device__ __forceinline__ uint64_t muldiv_floor(uint64_t a, uint64_t f, uint64_
     return est;
 }
 
+#ifdef DABS_TIMING
+// diagnostic build only (-DDABS_TIMING): per bucket (main phase of algorithm 0-4,
+// 5 = Straight/Greedy) SM cycles of thread 0 in [selection, wait for the first
+// row piece, rest of transfer + update, loop head], and flips
+__device__ unsigned long long g_tstat[6][5];
+__device__ unsigned long long g_tstat2[10];   // MaxMin/PositiveMin selection sub-steps
+#define DABS_TS(k) do { if (t == 0) { const long long now_ = clock64(); ts2_s[k] += now_ - tlast; tlast = now_; } } while (0)
+#else
+#define DABS_TS(k) do { } while (0)
+#endif
+
 template <int C, int NTT, int CL, bool TRACE>
 __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_kernel(const BatchParams p)
 {
@@ -411,19 +422,27 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
             d[8 * c + 4] = b.x; d[8 * c + 5] = b.y; d[8 * c + 6] = b.z; d[8 * c + 7] = b.w;
         }
     }
-    // sigma(x_k) as signed bytes, 4 elements per word: the int8 operand of the
-    // IDP.2A dot products that apply Eq.(4) (one instruction per element).
-    // Registers for one warp per search; shared memory ([EPT/16][NT] uint4,
-    // conflict-free) for the CTA tier, where registers are the limit.
+    // sigma(x_k) as signed bytes (0x01 = +1, 0xFF = -1), 4 elements per word:
+    // the int8 operand of the IDP.2A dot products that apply Eq.(4).  One warp
+    // per search: in registers.  CTA tiers (registers are the limit): in shared
+    // memory, [2][ceil(C/2)][NT] uint4 (16 bytes = two chunks per thread,
+    // conflict-free), copy 0 as is for sigma(x_i) = +1 and copy 1 negated for
+    // sigma(x_i) = -1, so the update needs no per-word negation.
     uint32_t sg[MW ? 1 : EPT / 4];
     uint4* sgs = reinterpret_cast<uint4*>(dyn_smem + 3 * nl);
+    constexpr int SGC = ((C + 1) / 2) << lgNT;   // uint4s per copy
 #pragma unroll
     for (int g = 0; g < EPT / 4; g++) {
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < 4; j++) w |= (((xb >> (4 * g + j)) & 1) ? 0x01u : 0xFFu) << (8 * j);
-        if constexpr (MW) reinterpret_cast<uint32_t*>(sgs)[(((g >> 2) << lgNT) + t) * 4 + (g & 3)] = w;
-        else sg[g] = w;
+        if constexpr (MW) {
+            uint32_t* s32 = reinterpret_cast<uint32_t*>(sgs);
+            s32[(((g >> 2) << lgNT) + t) * 4 + (g & 3)] = w;
+            s32[(SGC + ((g >> 2) << lgNT) + t) * 4 + (g & 3)] = w ^ 0xFEFEFEFEu;
+        } else {
+            sg[g] = w;
+        }
     }
     if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
     if (t == 0) {
@@ -498,10 +517,26 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
 
     // RandomMin candidates of main step ttv at batch flip fl (R-8): u16(k) = half
     // (k mod 2) of lowbias32(K + (k/2) * 0x9E3779B9), K = one Philox word per flip
+    // The main rule's Philox draw of batch step fl (R-6, R-8, R-9): every warp
+    // computes the draws of 32 consecutive steps at once, lane j holding step
+    // base + j, and hands out the one a step needs with a shuffle (one Philox
+    // per lane per 32 flips instead of one per thread per flip).
+    const uint32_t pur = algo == ALG_MAXMIN ? PUR_MAXMIN : (algo == ALG_RANDOM ? PUR_RANDMIN : PUR_POSMIN);
+    int rng_base = -1;
+    uint32_t rng_x = 0, rng_y = 0;
+    auto draw = [&](int fl) -> uint2 {
+        if ((fl >> 5) != rng_base) {
+            rng_base = fl >> 5;
+            const uint4 r = rng4(p.seed, pur, 0, gslot, p.gen, (uint32_t)((rng_base << 5) + lane));
+            rng_x = r.x;
+            rng_y = r.y;
+        }
+        return make_uint2(__shfl_sync(FULL, rng_x, fl & 31), __shfl_sync(FULL, rng_y, fl & 31));
+    };
     auto rand_cand = [&](int ttv, int fl) -> bits_t {
         const uint32_t p16 = (uint32_t)p.ptab[ttv];
         if (p16 >= 65536u) return vb;
-        const uint32_t K = rng4(p.seed, PUR_RANDMIN, 0, gslot, p.gen, (uint32_t)fl).x;
+        const uint32_t K = draw(fl).x;
         bits_t cand = 0;
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -518,14 +553,28 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
     };
     // (MW) the next main step's draws, computed while the row is in flight
     int pre_for = -1;
+
     bits_t cand_pre = 0;
-    uint4 r_pre = make_uint4(0, 0, 0, 0);
     for (int j = 0; j < tabu; j++) {
         const int r = ring_s[j];
         if (r >= 0 && owns(r)) { tcnt[lidx(r)]++; tm |= ONE << lbit(r); }
     }
 
+#ifdef DABS_TIMING
+    __shared__ unsigned int ts_s[6][5];
+    __shared__ unsigned int ts2_s[10];
+    long long tlast = 0;
+    if (t == 0) {
+        for (int j = 0; j < 30; j++) (&ts_s[0][0])[j] = 0u;
+        for (int j = 0; j < 10; j++) ts2_s[j] = 0u;
+    }
+    long long tA = clock64(), tB = 0, tC = 0, tD = tA;
+    int tbk = 5;
+#endif
     while (true) {
+#ifdef DABS_TIMING
+        tA = clock64();
+#endif
         // ---------------- phase transitions
         if (phase == 2 && tt == (algo == ALG_TWO ? 2 * n - 1 : T)) {
             phase = 1;
@@ -563,7 +612,8 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
                         if (hi2 > 0) wm |= (bits_t)((1u << hi2) - 1u) << (8 * c);
                     }
                 }
-                cursor = (cursor + w) % n;
+                cursor += w;                                       // w <= n: one conditional subtract
+                if (cursor >= n) cursor -= n;
                 M1 = wm & ~tm;
                 M2 = wm;
                 fb = 1;
@@ -778,15 +828,14 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
             }
             int v[4] = {tg, a1, a2, el != 0};
             const int ops[4] = {OP_MIN, OP_MIN, OP_MAX, OP_OR};
+            DABS_TS(0);
             block_reduce<MW>(v, ops, red_s, rc, lane, wid, NW);
             cl_combine(v, ops);
+            DABS_TS(1);
             gmin = v[0];
             bits_t EL = el;
             int thr;
-            const uint4 r = (MW && pre_for == flips)
-                                ? r_pre
-                                : rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
-                                       (uint32_t)flips);
+            const uint2 r = draw(flips);
             if (!v[3]) {
                 // every bit tabu: drop tabu (R-11)
                 EL = vb;
@@ -814,6 +863,7 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
                 u = r.x;
             }
             // count candidates (Delta <= thr, eligible) per chunk, packed 2 x 16 bits per word
+            DABS_TS(2);
             uint32_t pk[CW];
 #pragma unroll
             for (int w = 0; w < CW; w++) pk[w] = 0;
@@ -835,6 +885,7 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
                     pk[c >> 1] += (uint32_t)__popc(byte) << (16 * (c & 1));
                 }
             }
+            DABS_TS(3);
             uint32_t wt[CW];
 #pragma unroll
             for (int w = 0; w < CW; w++) wt[w] = warp_add(pk[w]);
@@ -867,6 +918,7 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
 #pragma unroll
                 for (int w = 0; w < CW; w++) bo[w] = (uint32_t)o[w];
             }
+            DABS_TS(4);
             uint32_t tot = 0;
 #pragma unroll
             for (int c = 0; c < C; c++)
@@ -892,39 +944,44 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
                 else { locate = r1 >= c0; r1 -= c0; }
             }
             // which warp holds rank r1 of chunk cs
+            DABS_TS(5);
             int wsel = locate ? 0 : -1;
             if (MW && locate) {
-                int x = lane < NW ? (int)(((uint32_t)red_s[par][lane][cs >> 1] >> (16 * (cs & 1))) & 0xFFFFu) : 0;
-                int y = x;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int z = __shfl_up_sync(FULL, y, off);
-                    if (lane >= off) y += z;
-                }
-                const unsigned bal = __ballot_sync(FULL, y > r1);
-                wsel = __ffs(bal) - 1;
-                r1 -= __shfl_sync(FULL, y - x, wsel);
+                // every warp: the chunk-cs count of the warps before it (one redux)
+                // and its own; the warp whose range holds rank r1 locates it
+                const int x = lane < NW ? (int)(((uint32_t)red_s[par][lane][cs >> 1] >> (16 * (cs & 1))) & 0xFFFFu) : 0;
+                const int pre = (int)warp_add(lane < wid ? (uint32_t)x : 0u);
+                const int own = __shfl_sync(FULL, x, wid);
+                wsel = (r1 >= pre && r1 < pre + own) ? wid : -1;
+                r1 -= pre;
             }
+            DABS_TS(6);
             int gi = -1, lv = 0, lx = 0;
             if (wid == wsel) {
                 uint32_t mybyte = 0;
-#pragma unroll
-                for (int c = 0; c < C; c++)
-                    if (c == cs) {
-#pragma unroll
-                        for (int e = 0; e < 8; e++) mybyte |= (uint32_t)(d[8 * c + e] <= thr) << e;
-                        mybyte &= (uint32_t)(EL >> (8 * c)) & 0xFFu;
-                    }
-                const int x = __popc(mybyte);
-                int y = x;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int z = __shfl_up_sync(FULL, y, off);
-                    if (lane >= off) y += z;
+                switch (cs) {
+#define DABS_MYBYTE(cc)                                                                           \
+    case cc:                                                                                      \
+        if constexpr (cc < C) {                                                                   \
+            _Pragma("unroll") for (int e = 0; e < 8; e++) mybyte |= (uint32_t)(d[8 * cc + e] <= thr) << e; \
+            mybyte &= (uint32_t)(EL >> (8 * cc)) & 0xFFu;                                         \
+        }                                                                                         \
+        break;
+                    DABS_MYBYTE(0) DABS_MYBYTE(1) DABS_MYBYTE(2) DABS_MYBYTE(3)
+                    DABS_MYBYTE(4) DABS_MYBYTE(5) DABS_MYBYTE(6) DABS_MYBYTE(7)
+#undef DABS_MYBYTE
+                default: break;
                 }
-                if (r1 >= y - x && r1 < y) {
+                // rank of this lane's first candidate in index order (lane-major,
+                // then element): per-bit ballots instead of a shuffle scan
+                const uint32_t lt = (1u << lane) - 1u;
+                int y0 = 0;
+#pragma unroll
+                for (int e = 0; e < 8; e++) y0 += __popc(__ballot_sync(FULL, (mybyte >> e) & 1u) & lt);
+                const int x = __popc(mybyte);
+                if (r1 >= y0 && r1 < y0 + x) {
                     uint32_t byte = mybyte;
-                    for (int j = 0; j < r1 - (y - x); j++) byte &= byte - 1;
+                    for (int j = 0; j < r1 - y0; j++) byte &= byte - 1;
                     const int e = __ffs(byte) - 1;
                     const int li = 8 * cs + e;
                     gi = gidx(cs, e);
@@ -994,10 +1051,16 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
         }
 
         // ---------------- Step 3: flip bit si, Eqs.(4)-(5)
+#ifdef DABS_TIMING
+        tB = clock64();
+        tbk = phase == 2 ? algo : 5;
+        if (t == 0 && rank == 0) { ts_s[tbk][0] += tB - tA; ts_s[tbk][3] += tA - tD; ts_s[tbk][4] += 1; }
+#endif
         // every thread has passed the last exchange: the row buffer is free
         const bool pre_issued = MW && CL == 1 && kind == 1;
         if (pre_issued) {
             mbar_wait(&mbar[0], par_row);
+            DABS_TS(7);
             si = sel_s[0]; sv = sel_s[1]; sx = sel_s[2];
         } else if (t == 0) {
             issue_row(si);
@@ -1006,13 +1069,18 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
         const int rmax_si = p.rmax[si];   // consumed after the update: its latency hides there
         // sigma(x_i) = -1 (x_i = 0 before the flip): negate every sigma(x_k) byte
         const uint32_t cmask = sx ? 0u : 0xFEFEFEFEu;
+        const uint4* sgn = sgs + (sx ? 0 : SGC);   // CTA tiers: the sign copy for sigma(x_i)
         if (__any_sync(FULL, owns(si))) {
             if (owns(si)) {
                 const int kk = lbit(si);
                 if constexpr (MW) {
                     neg_at(d, kk);               // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
+                    // sigma(x_k) byte of element kk in both sign copies
+                    uint8_t* b8 = reinterpret_cast<uint8_t*>(sgs);
                     const int g = kk >> 2;
-                    reinterpret_cast<uint8_t*>(sgs)[((((g >> 2) << lgNT) + t) * 4 + (g & 3)) * 4 + (kk & 3)] ^= 0xFEu;
+                    const int off = ((((g >> 2) << lgNT) + t) * 4 + (g & 3)) * 4 + (kk & 3);
+                    b8[off] ^= 0xFEu;
+                    b8[off + SGC * 16] ^= 0xFEu;
                 } else {
                     owner_flip(d, sg, kk);       // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
                 }
@@ -1037,50 +1105,65 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
         }
         flips++;
         if constexpr (MW) {
-            if (phase == 2 && tt < T && algo != ALG_CYCLIC && algo != ALG_TWO) {
-                if (algo == ALG_RANDOM) cand_pre = rand_cand(tt + 1, flips);
-                else r_pre = rng4(p.seed, algo == ALG_MAXMIN ? PUR_MAXMIN : PUR_POSMIN, 0, gslot, p.gen,
-                                  (uint32_t)flips);
+            if (phase == 2 && tt < T && algo == ALG_RANDOM) {
+                cand_pre = rand_cand(tt + 1, flips);
                 pre_for = flips;
             }
         }
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) {
             mbar_wait(&mbar[qq], par_row);
+#ifdef DABS_TIMING
+            if (qq == 0) tC = clock64();
+#endif
             uint4 rw[CPP];
 #pragma unroll
             for (int cc = 0; cc < CPP; cc++) rw[cc] = row_s[((qq * CPP + cc) << lgNT) + t];
-            uint4 sw[(CPP + 1) / 2];
             if constexpr (MW) {
+                uint4 sw[(CPP + 1) / 2];
 #pragma unroll
-                for (int j = 0; j < (CPP + 1) / 2; j++) sw[j] = sgs[(((qq * CPP) / 2 + j) << lgNT) + t];
-            }
+                for (int j = 0; j < (CPP + 1) / 2; j++) sw[j] = sgn[(((qq * CPP) / 2 + j) << lgNT) + t];
 #pragma unroll
-            for (int cc = 0; cc < CPP; cc++) {
-                const int c = qq * CPP + cc;
-                // Eq.(4): Delta_k += W_ik sigma(x_i) sigma(x_k); the row word holds
-                // (W_i,k0, W_i,k1) as int16x2, B holds (s_k0, 0, 0, s_k1) as int8x4
-                uint32_t g0, g1;
-                if constexpr (MW) {
+                for (int cc = 0; cc < CPP; cc++) {
+                    const int c = qq * CPP + cc;
+                    // Eq.(4): Delta_k += W_ik sigma(x_i) sigma(x_k); the row word holds
+                    // (W_i,k0, W_i,k1) as int16x2, B holds (+-s_k0, 0, 0, +-s_k1) as int8x4
                     const uint4 q4 = sw[cc >> 1];
-                    g0 = ((c & 1) ? q4.z : q4.x) ^ cmask;
-                    g1 = ((c & 1) ? q4.w : q4.y) ^ cmask;
-                } else {
-                    g0 = sg[2 * c] ^ cmask;
-                    g1 = sg[2 * c + 1] ^ cmask;
+                    const uint32_t g0 = (c & 1) ? q4.z : q4.x, g1 = (c & 1) ? q4.w : q4.y;
+                    const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
+                    const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
+                    d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);
+                    d[8 * c + 1] = __dp2a_hi((int)rw[cc].x, (int)B0, d[8 * c + 1]);
+                    d[8 * c + 2] = __dp2a_lo((int)rw[cc].y, (int)B1, d[8 * c + 2]);
+                    d[8 * c + 3] = __dp2a_hi((int)rw[cc].y, (int)B1, d[8 * c + 3]);
+                    d[8 * c + 4] = __dp2a_lo((int)rw[cc].z, (int)B2, d[8 * c + 4]);
+                    d[8 * c + 5] = __dp2a_hi((int)rw[cc].z, (int)B2, d[8 * c + 5]);
+                    d[8 * c + 6] = __dp2a_lo((int)rw[cc].w, (int)B3, d[8 * c + 6]);
+                    d[8 * c + 7] = __dp2a_hi((int)rw[cc].w, (int)B3, d[8 * c + 7]);
                 }
-                const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
-                const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
-                d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);
-                d[8 * c + 1] = __dp2a_hi((int)rw[cc].x, (int)B0, d[8 * c + 1]);
-                d[8 * c + 2] = __dp2a_lo((int)rw[cc].y, (int)B1, d[8 * c + 2]);
-                d[8 * c + 3] = __dp2a_hi((int)rw[cc].y, (int)B1, d[8 * c + 3]);
-                d[8 * c + 4] = __dp2a_lo((int)rw[cc].z, (int)B2, d[8 * c + 4]);
-                d[8 * c + 5] = __dp2a_hi((int)rw[cc].z, (int)B2, d[8 * c + 5]);
-                d[8 * c + 6] = __dp2a_lo((int)rw[cc].w, (int)B3, d[8 * c + 6]);
-                d[8 * c + 7] = __dp2a_hi((int)rw[cc].w, (int)B3, d[8 * c + 7]);
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < CPP; cc++) {
+                    const int c = qq * CPP + cc;
+                    // Eq.(4) as above; B holds (s_k0, 0, 0, s_k1) as int8x4, byte-permuted here
+                    const uint32_t g0 = sg[2 * c] ^ cmask, g1 = sg[2 * c + 1] ^ cmask;
+                    const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
+                    const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
+                    d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);
+                    d[8 * c + 1] = __dp2a_hi((int)rw[cc].x, (int)B0, d[8 * c + 1]);
+                    d[8 * c + 2] = __dp2a_lo((int)rw[cc].y, (int)B1, d[8 * c + 2]);
+                    d[8 * c + 3] = __dp2a_hi((int)rw[cc].y, (int)B1, d[8 * c + 3]);
+                    d[8 * c + 4] = __dp2a_lo((int)rw[cc].z, (int)B2, d[8 * c + 4]);
+                    d[8 * c + 5] = __dp2a_hi((int)rw[cc].z, (int)B2, d[8 * c + 5]);
+                    d[8 * c + 6] = __dp2a_lo((int)rw[cc].w, (int)B3, d[8 * c + 6]);
+                    d[8 * c + 7] = __dp2a_hi((int)rw[cc].w, (int)B3, d[8 * c + 7]);
+                }
             }
         }
+#ifdef DABS_TIMING
+        tD = clock64();
+        if (t == 0 && rank == 0) { ts_s[tbk][1] += tC - tB; ts_s[tbk][2] += tD - tC; }
+#endif
         par_row ^= 1u;
         glb = min(glb - (int64_t)rmax_si, (int64_t)-sv);
     }
@@ -1107,6 +1190,12 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
             atomicAdd(p.flip_total, (unsigned long long)flips);
         }
     }
+#ifdef DABS_TIMING
+    if (t == 0 && rank == 0)
+        for (int j = 0; j < 30; j++) atomicAdd(&g_tstat[0][0] + j, (unsigned long long)(&ts_s[0][0])[j]);
+    if (t == 0 && rank == 0)
+        for (int j = 0; j < 10; j++) atomicAdd(&g_tstat2[j], (unsigned long long)ts2_s[j]);
+#endif
     if constexpr (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still write to it
 }
 

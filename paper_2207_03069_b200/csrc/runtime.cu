@@ -147,6 +147,19 @@ extern "C" void dabs_config_default(dabs_config* cfg)
 
 extern "C" const char* dabs_last_error(void) { return g_err.c_str(); }
 
+#ifdef DABS_TIMING
+// diagnostic build only: read (and clear) the batch kernel's cycle buckets
+extern "C" int dabs_timing_read(unsigned long long* out)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_tstat, sizeof(g_tstat));
+    cudaMemcpyFromSymbol(out + 30, g_tstat2, sizeof(g_tstat2));
+    static const unsigned long long zero[30] = {};
+    cudaMemcpyToSymbol(g_tstat2, zero, sizeof(g_tstat2));
+    return (int)cudaMemcpyToSymbol(g_tstat, zero, sizeof(g_tstat));
+}
+#endif
+
 static int flip_factor(uint32_t milli, int n)
 {
     const int64_t v = ((int64_t)milli * n + 999) / 1000;
@@ -183,10 +196,10 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
 }
 static BatchFn pick_batch(const dabs_ctx* c, bool trace) { return pick_batch(c->C, c->NT, c->CL, trace); }
 
-// per CTA: its part of one W row + tabu counts (+ sigma bytes, CTA tiers)
+// per CTA: its part of one W row + tabu counts (+ two copies of the sigma bytes, CTA tiers)
 static size_t row_smem(const dabs_ctx* c)
 {
-    return (size_t)(c->mw ? 4 : 3) * (c->n_pad / c->CL);
+    return (size_t)(c->mw ? 5 : 3) * (c->n_pad / c->CL);
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
