@@ -694,21 +694,25 @@ void orc_build_target(int genop, const uint8_t* A, const uint8_t* Bp, const uint
     }
 }
 
-/* GA seeding for one slot (R-15, R-17, R-20, R-23). */
-static void ga_seed(world_t* w, int s)
+/* GA seeding for one slot (R-15, R-17, R-20, R-23).  `gen` is the
+   Philox generation field: the generation (bulk-synchronous schedule) or the
+   slot's batch index (asynchronous schedule, R-29).  `live_ring`: the last
+   pool's Xrossover partner is local pool 0 as it is now (R-29) instead of the
+   successor snapshot (R-23). */
+static void ga_seed_g(world_t* w, int s, uint32_t gen, int live_ring)
 {
     int n = w->n, cap = w->cap;
     int p = s / w->S;
     uint32_t gs = (uint32_t)(w->rank * w->P * w->S + s);
     const pool_t* pool = &w->pools[p];
-    const pool_t* succ = (p + 1 < w->P) ? &w->pools[p + 1] : &w->nbr;
+    const pool_t* succ = (p + 1 < w->P) ? &w->pools[p + 1] : (live_ring ? &w->pools[0] : &w->nbr);
     uint32_t a[4], b[4];
-    rng4(w->seed, PUR_GA_CHOICE, 0, gs, w->gen, 0, a);
+    rng4(w->seed, PUR_GA_CHOICE, 0, gs, gen, 0, a);
     int genop = (a[0] < w->eps_thr) ? w->gens[pick(a[1], (uint32_t)w->n_gen)]
                                     : pool->genop[pick(a[1], (uint32_t)cap)];
     int algo = (a[2] < w->eps_thr) ? w->algs[pick(a[3], (uint32_t)w->n_alg)]
                                    : pool->algo[pick(a[3], (uint32_t)cap)];
-    rng4(w->seed, PUR_GA_PARENT, 0, gs, w->gen, 0, b);
+    rng4(w->seed, PUR_GA_PARENT, 0, gs, gen, 0, b);
     uint32_t r1 = rank_pick(b[0], (uint32_t)cap), r2 = rank_pick(b[1], (uint32_t)cap);
     const uint8_t* A = pool->X + (size_t)r1 * n;
     const uint8_t* Bp = (genop == GEN_XROSSOVER ? succ->X : pool->X) + (size_t)r2 * n;
@@ -718,11 +722,13 @@ static void ga_seed(world_t* w, int s)
     uint32_t L = lo + pick(b[2], hi - lo + 1);
     uint32_t start = pick(b[3], (uint32_t)n);
     uint8_t* D = w->D + (size_t)s * n;
-    orc_build_target(genop, A, Bp, pool->X, n, w->seed, gs, w->gen, L, start, D);
+    orc_build_target(genop, A, Bp, pool->X, n, w->seed, gs, gen, L, start, D);
     w->palgo[s] = (uint8_t)algo;
     w->pgenop[s] = (uint8_t)genop;
     w->dispatch[((size_t)p * N_ALG + algo) * N_GEN + genop]++;
 }
+
+static void ga_seed(world_t* w, int s) { ga_seed_g(w, s, w->gen, 0); }
 
 /* merge one pool (R-18): stable sort of old ++ new by (E, seq),
    drop results equal in (E, X) to an earlier finite entry, keep `cap`. */
@@ -736,19 +742,19 @@ static int cand_cmp(const void* a, const void* b)
     return 0;
 }
 
-static void merge_pool(world_t* w, int p)
+/* merge the results of slots slot[0..m-1] (their packets) with sequence
+   numbers seqs[] into pool p */
+static void merge_results(world_t* w, int p, const int* slot, const uint64_t* seqs, int m)
 {
-    int n = w->n, cap = w->cap, S = w->S;
+    int n = w->n, cap = w->cap;
     pool_t* pool = &w->pools[p];
-    int M = cap + S;
+    int M = cap + m;
     cand_t* c = (cand_t*)malloc(sizeof(cand_t) * M);
     for (int r = 0; r < cap; r++) { c[r].E = pool->E[r]; c[r].seq = pool->seq[r]; c[r].src = -(r + 1); }
-    for (int j = 0; j < S; j++) {
-        int s = p * S + j;
-        uint32_t gs = (uint32_t)(w->rank * w->P * S + s);
-        c[cap + j].E = w->rE[s];
-        c[cap + j].seq = ((uint64_t)(w->gen + 1) << 32) | gs;
-        c[cap + j].src = s;
+    for (int j = 0; j < m; j++) {
+        c[cap + j].E = w->rE[slot[j]];
+        c[cap + j].seq = seqs[j];
+        c[cap + j].src = slot[j];
     }
     qsort(c, M, sizeof(cand_t), cand_cmp);
     pool_t np;
@@ -780,6 +786,22 @@ static void merge_pool(world_t* w, int p)
     free(c);
 }
 
+/* the generation's merge: pool p takes its S slots' results, in slot order,
+   with seq = (generation+1)<<32 | global slot */
+static void merge_pool(world_t* w, int p)
+{
+    int S = w->S;
+    int* slot = (int*)malloc(sizeof(int) * S);
+    uint64_t* seqs = (uint64_t*)malloc(sizeof(uint64_t) * S);
+    for (int j = 0; j < S; j++) {
+        slot[j] = p * S + j;
+        seqs[j] = ((uint64_t)(w->gen + 1) << 32) | (uint32_t)(w->rank * w->P * S + slot[j]);
+    }
+    merge_results(w, p, slot, seqs, S);
+    free(slot);
+    free(seqs);
+}
+
 /* The local part of one generation: GA seeding for every slot, one batch per
    slot (slot order), then the per-pool merge.  Returns 0 or an error. */
 int orc_world_generation_local(void* vw)
@@ -801,6 +823,65 @@ int orc_world_generation_local(void* vw)
     }
     for (int p = 0; p < w->P; p++) merge_pool(w, p);
     return 0;
+}
+
+/* Asynchronous schedule (reading R-29), replayed from a log.
+   The paper's host hands each block a new packet as soon as its previous batch
+   returns; there is no generation barrier.  Each slot s
+   runs batches k = 0, 1, 2, ...; batch k uses the Philox generation field k.
+   Every slot's packet 0 is seeded from the freshly initialised pools (k = 0)
+   before any batch.  log[e] = s | seeded<<31 is the e-th merge event, in the
+   order the device serialised them: slot s's current batch result enters its
+   pool as one result with seq = (e+1)<<32 | global slot (rule R-18 with one
+   newcomer); the run best and its record (event index as `generation`) are
+   updated on strict improvement; then, if `seeded`, packet k+1 is drawn from
+   the pools as they are after this merge, with the last pool's Xrossover
+   partner = local pool 0, live (R-29).  Single rank only.
+   Returns 0, or 20 (bad slot), 21 (event after the slot's last batch),
+   22 (a slot without a final unseeded event), or a batch error. */
+int orc_world_async_replay(void* vw, const uint32_t* log, int64_t len)
+{
+    world_t* w = (world_t*)vw;
+    int n = w->n, ns = w->P * w->S;
+    if (w->world != 1) return 23;
+    uint32_t* k = (uint32_t*)calloc(ns, sizeof(uint32_t));
+    uint8_t* done = (uint8_t*)calloc(ns, 1);
+    int err = 0;
+    for (int s = 0; s < ns; s++) ga_seed_g(w, s, 0, 1);
+    for (int64_t e = 0; e < len && !err; e++) {
+        int s = (int)(log[e] & 0x7FFFFFFFu);
+        int seeded = (int)(log[e] >> 31);
+        if (s >= ns) { err = 20; break; }
+        if (done[s]) { err = 21; break; }
+        uint32_t gs = (uint32_t)s;
+        err = orc_batch(w->U, n, w->T, w->B, w->tabu,
+                        w->sx + (size_t)s * n, w->sdelta + (size_t)s * n, &w->sE[s],
+                        w->sring + (size_t)s * ORC_TABU_MAX,
+                        w->D + (size_t)s * n, w->palgo[s], w->seed, gs, k[s],
+                        w->rbest + (size_t)s * n, &w->rE[s], &w->rflips[s],
+                        NULL, NULL, NULL, 0, w->checked);
+        if (err) break;
+        w->total_flips += (uint64_t)w->rflips[s];
+        uint64_t seq = ((uint64_t)(e + 1) << 32) | gs;
+        merge_results(w, s / w->S, &s, &seq, 1);
+        if (w->rE[s] < w->best_E) {
+            w->best_E = w->rE[s];
+            memcpy(w->best_X, w->rbest + (size_t)s * n, n);
+            w->best_algo = w->palgo[s]; w->best_genop = w->pgenop[s];
+            w->best_gen = e; w->best_slot = gs;
+        }
+        if (seeded) {
+            k[s]++;
+            ga_seed_g(w, s, k[s], 1);
+        } else {
+            done[s] = 1;
+        }
+    }
+    for (int s = 0; s < ns && !err; s++) if (!done[s]) err = 22;
+    free(k);
+    free(done);
+    if (err) w->err = err;
+    return err;
 }
 
 /* Exchange payload (oracle format): first local pool + this rank's best

@@ -90,6 +90,8 @@ def lib():
         L.orc_world_get_packet.argtypes = [P, C.c_int, P, P, P, P, P, P]
         L.orc_world_get_stats.argtypes = [P, P, P]
         L.orc_world_get_best.argtypes = [P, P, P, P]
+        L.orc_world_async_replay.argtypes = [P, P, C.c_int64]
+        L.orc_world_async_replay.restype = C.c_int
         L.orc_lowbias32.argtypes = [u32]
         L.orc_lowbias32.restype = u32
         L.orc_rank_pick.argtypes = [u32, u32]
@@ -309,6 +311,14 @@ class World:
         err = lib().orc_world_generation_local(self.h)
         if err:
             raise RuntimeError(f"oracle generation error {err}")
+
+    def async_replay(self, log) -> None:
+        """Replay an asynchronous-schedule event log (R-29) from a
+        fresh reset: entries s | seeded<<31 in merge order."""
+        lg = np.ascontiguousarray(np.asarray(log, dtype=np.uint32))
+        err = lib().orc_world_async_replay(self.h, _p(lg), int(lg.size))
+        if err:
+            raise RuntimeError(f"oracle async replay error {err}")
 
     def export(self) -> np.ndarray:
         buf = np.zeros(self.payload_bytes, np.uint8)
