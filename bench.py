@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
+    ap.add_argument("--no-async", action="store_true", help="skip the asynchronous-schedule line (SURVEY f1)")
     return ap.parse_args()
 
 
@@ -344,6 +345,35 @@ def main():
                                  "success_rate": len(ok) / len(tts),
                                  "mean_tts_s": float(np.mean(ok)) if ok else None, "limit_s": 20,
                                  "timer": "host wall clock from dabs_reset to the generation that found it"}
+    # ---- asynchronous schedule: the same workload and seed
+    # through dabs_run_async -- one persistent kernel, one CTA per resident
+    # search, no generation barrier -- for the same flips as the timed steps.
+    # Kernel time by CUDA events on the library's stream (batch_ms_last).
+    if world == 1 and not args.no_async and solver.threads * 1 <= 512 and n <= 32768:
+        sa = Solver(None if csr else U, csr=csr, s_milli=meta["s_milli"], b_milli=meta["b_milli"],
+                    pools=meta.get("pools", 1), one_wave=True, device=torch.cuda.current_device(),
+                    stream=stream.cuda_stream)
+        budget = int(sum(local_flips))
+        sa.run_async(args.seed, max(1, budget // 4))   # warm-up
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+        t0 = time.perf_counter()
+        sa.run_async(args.seed, budget)
+        wall = time.perf_counter() - t0
+        sta = sa.stats()
+        wait_ns, hold_ns = sa.async_lock_ns()
+        out["async_schedule"] = {
+            "lock_hold_us_per_event": hold_ns / 1e3 / max(1, sta.generations),
+            "lock_wait_us_per_event": wait_ns / 1e3 / max(1, sta.generations),
+            "lock_busy_frac": hold_ns / 1e6 / max(1e-9, sta.batch_ms_last),
+            "value": sta.total_flips / (sta.batch_ms_last / 1e3), "unit": UNIT,
+            "wall_value": sta.total_flips / wall, "flips": int(sta.total_flips),
+            "merge_events": int(sta.generations), "slots": int(sa.slots), "kernel_ms": float(sta.batch_ms_last),
+            "vs_generation_schedule": (sta.total_flips / (sta.batch_ms_last / 1e3)) / value,
+            "what": "dabs_run_async: persistent kernel, one CTA per resident search, device-side pool lock, "
+                    "merge/seed per batch (no generation barrier); value = flips / kernel time"}
+        sa.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         f, dt, cores, quota = oracle_sample(U, meta, args.cpu_seconds, args.seed)
         out["cpu_baseline"] = {"value": f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",

@@ -86,8 +86,12 @@ typedef struct {
     uint32_t restart_gens;    /* restart-on-merge (R-28): after this many
                                  generations without a box-wide improvement, pools and
                                  slots start afresh (the best is kept); 0 = off (default) */
-    uint32_t reserved;
+    uint32_t flags;           /* DABS_FLAG_ONE_WAVE: slots_per_pool = 0 sizes ONE wave of
+                                 co-resident searches (the persistent CTAs of
+                                 dabs_run_async) instead of four waves per generation */
 } dabs_config;
+
+#define DABS_FLAG_ONE_WAVE 1u
 
 /* Fills the defaults listed above. */
 void dabs_config_default(dabs_config* cfg);
@@ -129,6 +133,37 @@ dabs_status dabs_generation(dabs_ctx* ctx);
  * with identical arguments. */
 dabs_status dabs_run(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t* best_x_host,
                      int64_t* best_e);
+
+/* Asynchronous schedule (reading R-29; the paper's
+ * packet flow without a generation barrier).
+ * dabs_reset(seed); packet 0 of every slot is seeded from the fresh pools;
+ * then ONE persistent kernel, one CTA per slot, runs batch after batch: after
+ * batch k a slot takes the rank's pool lock, merges its result into its pool
+ * (R-18 with one newcomer, seq = (event+1)<<32 | slot), updates the run best,
+ * appends (slot | seeded<<31) to the event log and, unless the run is
+ * stopping, seeds packet k+1 (Philox generation field = k+1) from the pools as
+ * they are (the last pool's Xrossover partner is local pool 0, live).  The
+ * run stops seeding once the merged flips >= flip_budget, best <=
+ * target_energy, or the time limit has passed (device clock); every slot then
+ * merges its running batch and exits.  Deterministic given the log: the CPU
+ * oracle replays it (orc_world_async_replay).  Slots are persistent CTAs, so
+ * create the context with flags = DABS_FLAG_ONE_WAVE (slots beyond the
+ * resident capacity start only after the stop).  Requires world == 1, the CTA
+ * tiers (n <= 32768), restart_gens == 0 and tracing off, else DABS_E_ARG.
+ * Writes the best vector (n bytes, host) and energy; dabs_get_stats then
+ * reports the run (generations = merge events, time_to_best_ns from the
+ * kernel's start on the device clock, batch_ms_last = the kernel's time). */
+dabs_status dabs_run_async(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t* best_x_host,
+                           int64_t* best_e);
+
+/* The last dabs_run_async's event log, in merge order: entry = local slot |
+ * (1<<31 if a next packet was seeded).  Copies min(cap, len) entries to `log`
+ * (host, caller-owned; may be NULL), *len = the number of events. */
+dabs_status dabs_async_log(const dabs_ctx* ctx, uint32_t* log, int64_t cap, int64_t* len);
+
+/* The last dabs_run_async's pool-lock profile (device clock): the sum over
+ * merge events of the time spent waiting for the lock and holding it. */
+dabs_status dabs_async_lock_ns(const dabs_ctx* ctx, uint64_t* wait_ns, uint64_t* hold_ns);
 
 /* Best vector and energy seen so far (box-wide after the last exchange). */
 dabs_status dabs_best(const dabs_ctx* ctx, uint8_t* best_x_host, int64_t* best_e);

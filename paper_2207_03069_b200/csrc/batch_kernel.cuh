@@ -361,8 +361,19 @@ __device__ unsigned long long g_tstat2[10];   // MaxMin/PositiveMin selection su
 #define DABS_TS(k) do { } while (0)
 #endif
 
-template <int C, int NTT, int CL, bool TRACE>
-__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_kernel(const BatchParams p)
+__device__ __forceinline__ void mbar_inval(uint64_t* m)
+{
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+
+// One batch search of slot s: load the slot's persistent state,
+// Straight(D) -> Greedy -> {main -> Greedy} until B flips, write back the
+// state and the result packet.  `gen` is the Philox generation field (the
+// generation, or the slot's batch index under the asynchronous schedule,
+// R-29).  REUSE: the CTA runs further batches afterwards (persistent kernel),
+// so the row mbarriers are invalidated at the end.
+template <int C, int NTT, int CL, bool TRACE, bool REUSE>
+__device__ __forceinline__ void batch_body(const BatchParams& p, const int s, const uint32_t gen)
 {
     static_assert(CL == 1 || (CL == 2 && NTT > 32), "cluster tier needs the CTA tier");
     constexpr bool MW = NTT > 32;                    // more than one warp per search
@@ -383,8 +394,6 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
     const int lane = t & 31, wid = t >> 5;
     const uint32_t rank = CL == 2 ? cluster_rank() : 0u;   // CTA within the search's cluster
     const int tq = (int)rank * NT + t;                      // thread within the search
-    const int sidx = (int)blockIdx.x / CL;
-    const int s = p.order ? p.order[sidx] : p.slot0 + sidx;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
     const int n = p.n;
 
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
     auto draw = [&](int fl) -> uint2 {
         if ((fl >> 5) != rng_base) {
             rng_base = fl >> 5;
-            const uint4 r = rng4(p.seed, pur, 0, gslot, p.gen, (uint32_t)((rng_base << 5) + lane));
+            const uint4 r = rng4(p.seed, pur, 0, gslot, gen, (uint32_t)((rng_base << 5) + lane));
             rng_x = r.x;
             rng_y = r.y;
         }
@@ -1197,6 +1206,21 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
         for (int j = 0; j < 10; j++) atomicAdd(&g_tstat2[j], (unsigned long long)ts2_s[j]);
 #endif
     if constexpr (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still write to it
+    if constexpr (REUSE) {
+        static_assert(CL == 1, "persistent batches: CTA tiers only");
+        if constexpr (MW) __syncthreads(); else __syncwarp();
+        if (t == 0)
+#pragma unroll
+            for (int qq = 0; qq < NP; qq++) mbar_inval(&mbar[qq]);
+    }
+}
+
+template <int C, int NTT, int CL, bool TRACE>
+__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_kernel(const BatchParams p)
+{
+    const int sidx = (int)blockIdx.x / CL;
+    const int s = p.order ? p.order[sidx] : p.slot0 + sidx;
+    batch_body<C, NTT, CL, TRACE, false>(p, s, p.gen);
 }
 
 }  // namespace dabs

@@ -154,9 +154,79 @@ __global__ void init_pools_kernel(GaConst g, PoolView* pools, uint32_t gid0, uin
 }
 
 // ------------------------------------------------------------------ a3 GA seeding
-// One warp per slot: adaptive choice of genop and algorithm (R-15),
-// rank-biased parents (R-17), one of the eight genetic operations
+// One warp seeds one slot: adaptive choice of genop and algorithm (P:600-615,
+// R-15), rank-biased parents (R-17), one of the genetic operations
 // (R-20; Xrossover P:628-630, R-23) -> target D and tags.
+// `ord` / `ord_succ` (may be NULL = identity) map a pool rank to its physical
+// row (asynchronous schedule, R-29); `ord` lives in shared memory, `ord_succ`
+// in global memory unless `succ_ord_shared`.  Pool reads go to L2 (ld.cg)
+// because other SMs may have written the pools during the same kernel.
+__device__ __forceinline__ void ga_seed_warp(const GaConst& g, const PoolView& pool, const int32_t* ord,
+                                             const PoolView& succ, const int32_t* ord_succ, bool succ_ord_shared,
+                                             int p, uint32_t gs, uint32_t gen, uint32_t* __restrict__ Dout,
+                                             uint8_t* palgo_s, uint8_t* pgenop_s,
+                                             unsigned long long* __restrict__ dispatch, int lane)
+{
+    auto row = [&](const int32_t* o, uint32_t r) { return o ? (uint32_t)o[r] : r; };
+    auto row_succ = [&](uint32_t r) {
+        return ord_succ ? (uint32_t)(succ_ord_shared ? ord_succ[r] : __ldcg(ord_succ + r)) : r;
+    };
+    const uint4 a = rng4(g.seed, PUR_GA_CHOICE, 0, gs, gen, 0);
+    const int genop = (a.x < g.eps_thr) ? g.gens[pick_u(a.y, (uint32_t)g.n_gen)]
+                                        : (int)__ldcg(pool.genop + row(ord, pick_u(a.y, (uint32_t)g.cap)));
+    const int algo = (a.z < g.eps_thr) ? g.algs[pick_u(a.w, (uint32_t)g.n_alg)]
+                                       : (int)__ldcg(pool.algo + row(ord, pick_u(a.w, (uint32_t)g.cap)));
+    const uint4 b = rng4(g.seed, PUR_GA_PARENT, 0, gs, gen, 0);
+    const uint32_t r1 = rank_pick(b.x, (uint32_t)g.cap), r2 = rank_pick(b.y, (uint32_t)g.cap);
+    const uint32_t* A = pool.X + (size_t)row(ord, r1) * g.nwp;
+    const uint32_t* Bv = genop == GEN_XROSSOVER ? succ.X + (size_t)row_succ(r2) * g.nwp
+                                                : pool.X + (size_t)row(ord, r2) * g.nwp;
+    const uint32_t* B0 = pool.X + (size_t)row(ord, 0) * g.nwp;   // the pool's best (GEN_BEST)
+    const uint32_t n = (uint32_t)g.n;
+    const uint32_t lo = n < 32u ? n : 32u;
+    const uint32_t hi = (n / 2 > lo) ? n / 2 : lo;
+    const uint32_t L = lo + pick_u(b.z, hi - lo + 1);
+    const uint32_t start = pick_u(b.w, n);
+    // IntervalZero segment as up to two index ranges [start, e0) and [0, e1)
+    const uint32_t e0 = min(start + L, n);
+    const int64_t e1 = (int64_t)start + L - n;
+    for (int w = lane; w < g.nwp; w += 32) {
+        const uint4 m = rng4(g.seed, PUR_GA_MASK, (uint32_t)w, gs, gen, 0);
+        const uint32_t p8 = m.x & m.y & m.z;
+        uint32_t v;
+        switch (genop) {
+        case GEN_MUTATION: v = __ldcg(A + w) ^ p8; break;
+        case GEN_CROSSOVER:
+        case GEN_XROSSOVER: v = (__ldcg(A + w) & m.x) | (__ldcg(Bv + w) & ~m.x); break;
+        case GEN_ZERO: v = __ldcg(A + w) & ~p8; break;
+        case GEN_ONE: v = __ldcg(A + w) | p8; break;
+        case GEN_INTERVALZERO: {
+            const int64_t base = (int64_t)w * 32;
+            uint32_t clr = 0;
+            int64_t lo1 = max((int64_t)start - base, (int64_t)0), hi1 = min((int64_t)e0 - base, (int64_t)32);
+            if (lo1 < hi1) clr |= (uint32_t)((((uint64_t)1 << (hi1 - lo1)) - 1) << lo1);
+            const int64_t hi2 = min(e1 - base, (int64_t)32);
+            if (hi2 > 0) clr |= (uint32_t)(((uint64_t)1 << hi2) - 1);
+            v = __ldcg(A + w) & ~clr;
+            break;
+        }
+        case GEN_BEST: v = __ldcg(B0 + w); break;
+        case GEN_MUTCROSS: v = ((__ldcg(A + w) & m.w) | (__ldcg(Bv + w) & ~m.w)) ^ p8; break;
+        default: v = m.x; break;   // GEN_RANDOM
+        }
+        const int64_t rem = (int64_t)n - (int64_t)w * 32;   // clear bits >= n
+        if (rem <= 0) v = 0;
+        else if (rem < 32) v &= (1u << rem) - 1u;
+        Dout[w] = v;
+    }
+    if (lane == 0) {
+        *palgo_s = (uint8_t)algo;
+        *pgenop_s = (uint8_t)genop;
+        atomicAdd(&dispatch[((size_t)p * N_ALG + algo) * N_GEN + genop], 1ull);
+    }
+}
+
+// One warp per slot, every slot of the generation (bulk-synchronous schedule).
 __global__ void ga_seed_kernel(GaConst g, const PoolView* __restrict__ pools, uint32_t slot_base,
                                uint32_t gen, int nslots, uint32_t* __restrict__ D,
                                uint8_t* __restrict__ palgo, uint8_t* __restrict__ pgenop,
@@ -167,61 +237,10 @@ __global__ void ga_seed_kernel(GaConst g, const PoolView* __restrict__ pools, ui
     const int lane = threadIdx.x & 31;
     if (s >= nslots) return;
     const int p = s / g.S;
-    const uint32_t gs = slot_base + (uint32_t)s;
     const PoolView pool = pools[p];
     const PoolView succ = pools[p + 1];      // pools[P] is the successor snapshot
-    const uint4 a = rng4(g.seed, PUR_GA_CHOICE, 0, gs, gen, 0);
-    const int genop = (a.x < g.eps_thr) ? g.gens[pick_u(a.y, (uint32_t)g.n_gen)]
-                                        : (int)pool.genop[pick_u(a.y, (uint32_t)g.cap)];
-    const int algo = (a.z < g.eps_thr) ? g.algs[pick_u(a.w, (uint32_t)g.n_alg)]
-                                       : (int)pool.algo[pick_u(a.w, (uint32_t)g.cap)];
-    const uint4 b = rng4(g.seed, PUR_GA_PARENT, 0, gs, gen, 0);
-    const uint32_t r1 = rank_pick(b.x, (uint32_t)g.cap), r2 = rank_pick(b.y, (uint32_t)g.cap);
-    const uint32_t* A = pool.X + (size_t)r1 * g.nwp;
-    const uint32_t* Bv = (genop == GEN_XROSSOVER ? succ.X : pool.X) + (size_t)r2 * g.nwp;
-    const uint32_t n = (uint32_t)g.n;
-    const uint32_t lo = n < 32u ? n : 32u;
-    const uint32_t hi = (n / 2 > lo) ? n / 2 : lo;
-    const uint32_t L = lo + pick_u(b.z, hi - lo + 1);
-    const uint32_t start = pick_u(b.w, n);
-    // IntervalZero segment as up to two index ranges [start, e0) and [0, e1)
-    const uint32_t e0 = min(start + L, n);
-    const int64_t e1 = (int64_t)start + L - n;
-    uint32_t* Dout = D + (size_t)s * g.nwp;
-    for (int w = lane; w < g.nwp; w += 32) {
-        const uint4 m = rng4(g.seed, PUR_GA_MASK, (uint32_t)w, gs, gen, 0);
-        const uint32_t p8 = m.x & m.y & m.z;
-        uint32_t v;
-        switch (genop) {
-        case GEN_MUTATION: v = A[w] ^ p8; break;
-        case GEN_CROSSOVER:
-        case GEN_XROSSOVER: v = (A[w] & m.x) | (Bv[w] & ~m.x); break;
-        case GEN_ZERO: v = A[w] & ~p8; break;
-        case GEN_ONE: v = A[w] | p8; break;
-        case GEN_INTERVALZERO: {
-            const int64_t base = (int64_t)w * 32;
-            uint32_t clr = 0;
-            int64_t lo1 = max((int64_t)start - base, (int64_t)0), hi1 = min((int64_t)e0 - base, (int64_t)32);
-            if (lo1 < hi1) clr |= (uint32_t)((((uint64_t)1 << (hi1 - lo1)) - 1) << lo1);
-            const int64_t hi2 = min(e1 - base, (int64_t)32);
-            if (hi2 > 0) clr |= (uint32_t)(((uint64_t)1 << hi2) - 1);
-            v = A[w] & ~clr;
-            break;
-        }
-        case GEN_BEST: v = pool.X[w]; break;
-        case GEN_MUTCROSS: v = ((A[w] & m.w) | (Bv[w] & ~m.w)) ^ p8; break;
-        default: v = m.x; break;   // GEN_RANDOM
-        }
-        const int64_t rem = (int64_t)n - (int64_t)w * 32;   // clear bits >= n
-        if (rem <= 0) v = 0;
-        else if (rem < 32) v &= (1u << rem) - 1u;
-        Dout[w] = v;
-    }
-    if (lane == 0) {
-        palgo[s] = (uint8_t)algo;
-        pgenop[s] = (uint8_t)genop;
-        atomicAdd(&dispatch[((size_t)p * N_ALG + algo) * N_GEN + genop], 1ull);
-    }
+    ga_seed_warp(g, pool, nullptr, succ, nullptr, false, p, slot_base + (uint32_t)s, gen, D + (size_t)s * g.nwp,
+                 palgo + s, pgenop + s, dispatch, lane);
 }
 
 // Launch order for the batch kernel: slots whose batches cost the most start

@@ -18,6 +18,7 @@
 #include "../../include/dabs.h"
 #include "batch_kernel.cuh"
 #include "ga_pool_kernels.cuh"
+#include "async_kernel.cuh"
 
 using namespace dabs;
 
@@ -97,6 +98,17 @@ struct dabs_ctx {
     uint64_t wall_ns = 0, ttb_ns = 0;
     float batch_ms = 0, ga_ms = 0, merge_ms = 0;
     cudaEvent_t ev[6] = {};
+    // asynchronous schedule
+    uint32_t* a_lock = nullptr;      // tickets [P*32], serving [P*32], evcount, stop, best lock (own lines)
+    uint64_t* a_hash = nullptr;      // [P][cap]
+    uint64_t a_wait_ns = 0, a_hold_ns = 0;   // last async run: summed pool-lock wait / hold (device clock)
+    uint32_t* a_log = nullptr;
+    uint32_t a_log_cap = 0;
+    unsigned long long* a_u64 = nullptr;   // flips_cum, t0, best_t
+    int64_t* a_bestE = nullptr;
+    uint32_t* a_bestX = nullptr;
+    int32_t* a_brec = nullptr;
+    std::vector<uint32_t> a_log_h;
     std::chrono::steady_clock::time_point t_reset;
 };
 
@@ -195,6 +207,19 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
     }
 }
 static BatchFn pick_batch(const dabs_ctx* c, bool trace) { return pick_batch(c->C, c->NT, c->CL, trace); }
+
+using AsyncFn = void (*)(const AsyncArgs);
+static AsyncFn pick_async(int C, int NT)
+{
+    switch (NT) {
+    case 32: return C == 1 ? async_kernel<1, 32> : C == 2 ? async_kernel<2, 32> : C == 4 ? async_kernel<4, 32>
+                                                                                 : async_kernel<8, 32>;
+    case 64: return async_kernel<8, 64>;
+    case 128: return async_kernel<8, 128>;
+    case 256: return async_kernel<8, 256>;
+    default: return async_kernel<8, 512>;
+    }
+}
 
 // per CTA: its part of one W row + tabu counts (+ two copies of the sigma bytes, CTA tiers)
 static size_t row_smem(const dabs_ctx* c)
@@ -307,6 +332,11 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
+    if (c->CL == 1) {
+        cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)row_smem(c));
+        if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
+    }
     c->T = flip_factor(cfg.s_milli, n);
     c->B = flip_factor(cfg.b_milli, n);
     c->tabu = (int)cfg.tabu_period;
@@ -316,12 +346,19 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         c->S = (int)cfg.slots_per_pool;
     } else {
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
+        const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) && c->CL == 1;
+        if (one_wave)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT), c->NT, row_smem(c));
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
-        c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
-                                                // (TwoNeighbor runs 2n-1 main flips), more
-                                                // waves let the block scheduler balance them
+        if (one_wave)
+            c->S = std::max(1, conc / c->P);    // persistent CTAs of the asynchronous schedule, all resident
+        else
+            c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
+                                                    // (TwoNeighbor runs 2n-1 main flips), more
+                                                    // waves let the block scheduler balance them
     }
     c->slots = c->P * c->S;
     if ((int64_t)c->slots * (cfg.world) >= (1ll << 31)) return bail(fail(DABS_E_ARG, "too many slots"));
@@ -447,6 +484,9 @@ static dabs_status create_end(dabs_ctx* c)
         L.oBestX = o; o = al8(o + 4 * nwp);
         L.bytes = o;
     }
+    AB(c->a_lock, 64 * P + 96); AB(c->a_hash, P * cap); AB(c->a_u64, 12); AB(c->a_bestE, 1); AB(c->a_bestX, nwp); AB(c->a_brec, 4);
+    c->a_log_cap = (uint32_t)std::max<size_t>(1u << 20, 64 * ns);
+    AB(c->a_log, c->a_log_cap);
     AB(c->send, c->L.bytes);
     AB(c->recv, c->L.bytes * (size_t)cfg.world);
 #undef AB
@@ -715,6 +755,106 @@ extern "C" dabs_status dabs_run(dabs_ctx* c, uint64_t seed, uint64_t flip_budget
         }
     }
     return dabs_best(c, best_x, best_e);
+}
+
+// Asynchronous schedule: one persistent kernel, no
+// generation barrier, every merge logged for the oracle's replay.
+extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_budget, uint8_t* best_x,
+                                      int64_t* best_e)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    if (c->cfg.world != 1) return fail(DABS_E_ARG, "the asynchronous schedule runs on one rank (world == 1)");
+    if (c->CL != 1) return fail(DABS_E_ARG, "the asynchronous schedule needs n <= 32768 (CTA tiers)");
+    if (c->cfg.restart_gens) return fail(DABS_E_ARG, "restart-on-merge is a generation-schedule option");
+    if (c->trace_slot >= 0) return fail(DABS_E_ARG, "tracing is a generation-schedule option");
+    dabs_status st = dabs_reset(c, seed);
+    if (st != DABS_OK) return st;
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t s0 = c->stream;
+    // packet 0 of every slot from the fresh pools
+    ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, s0>>>(c->ga, c->pools_d, 0u, 0u, c->slots, c->D, c->palgo,
+                                                        c->pgenop, c->dispatch);
+    CK(cudaGetLastError());
+    int32_t* ord = c->margs.acc;   // [P][cap] scratch, free outside the generation schedule's merge
+    CK(cudaMemsetAsync(c->a_lock, 0, 4 * (64 * (size_t)c->P + 96), s0));
+    CK(cudaMemsetAsync(c->a_u64, 0, 96, s0));
+    CK(cudaMemsetAsync(c->a_brec, 0xFF, 16, s0));
+    const int64_t inf = E_INF;
+    CK(cudaMemcpyAsync(c->a_bestE, &inf, 8, cudaMemcpyHostToDevice, s0));
+    async_init_kernel<<<4, 256, 0, s0>>>(ord, c->a_hash, c->P, c->cap, c->a_u64 + 1);
+    CK(cudaGetLastError());
+    AsyncArgs a{};
+    a.bp = batch_params(c, c->seed, 0u, 0);
+    a.g = c->ga;
+    a.pools = c->pools_d;
+    a.ord = ord;
+    a.hash = c->a_hash;
+    a.D = c->D; a.palgo = c->palgo; a.pgenop = c->pgenop;
+    a.dispatch = c->dispatch; a.inserted = c->inserted;
+    a.ticket = c->a_lock; a.serving = c->a_lock + 32 * c->P; a.evcount = c->a_lock + 64 * c->P;
+    a.stop = (int32_t*)(c->a_lock + 64 * c->P + 32); a.best_lock = (int32_t*)(c->a_lock + 64 * c->P + 64);
+    a.log = c->a_log; a.log_cap = c->a_log_cap; a.slots = c->slots;
+    a.flips_cum = c->a_u64; a.t0 = c->a_u64 + 1; a.best_t = c->a_u64 + 2; a.lock_ns = c->a_u64 + 3;
+    a.budget = flip_budget;
+    a.target = c->cfg.target_energy;
+    a.time_limit_ns = c->cfg.time_limit_ns;
+    a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
+    CK(cudaEventRecord(c->ev[1], s0));
+    pick_async(c->C, c->NT)<<<c->slots, c->NT, row_smem(c), s0>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[2], s0));
+    async_compact_kernel<<<c->P, 256, 0, s0>>>(c->pools_d, ord, c->cap, c->nwp, c->margs.sX, c->margs.sE,
+                                                c->margs.sSeq, c->margs.sAlgo, c->margs.sGenop);
+    CK(cudaGetLastError());
+    uint32_t nev = 0;
+    unsigned long long u64[12];
+    int64_t bE = E_INF;
+    int32_t rec[4];
+    std::vector<uint32_t> words(c->nwp);
+    CK(cudaMemcpyAsync(&nev, c->a_lock + 64 * c->P, 4, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(u64, c->a_u64, 96, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(&bE, c->a_bestE, 8, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(rec, c->a_brec, 16, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(words.data(), c->a_bestX, 4 * c->nwp, cudaMemcpyDeviceToHost, s0));
+    CK(cudaStreamSynchronize(s0));
+    cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
+    c->a_log_h.resize(nev);
+    if (nev) CK(cudaMemcpy(c->a_log_h.data(), c->a_log, 4 * (size_t)nev, cudaMemcpyDeviceToHost));
+    const auto t1 = std::chrono::steady_clock::now();
+    c->wall_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    c->total_flips = c->local_flips = u64[0];
+    c->gen = nev;
+    c->best_E = bE;
+    for (int k = 0; k < c->n; k++) c->best_X[k] = (uint8_t)((words[k >> 5] >> (k & 31)) & 1u);
+    for (int j = 0; j < 4; j++) c->rec[j] = rec[j];
+    c->ttb_ns = u64[2] > u64[1] ? u64[2] - u64[1] : 0;   // device clock, from the kernel's start
+    c->a_wait_ns = u64[3];
+    c->a_hold_ns = u64[4];
+    if (getenv("DABS_ASYNC_PHASES"))
+        fprintf(stderr, "async lock phases (us/event): A %.2f B %.2f dup+ins %.2f GA %.2f release %.2f\n",
+                u64[5] / 1e3 / std::max(1u, nev), u64[6] / 1e3 / std::max(1u, nev), u64[7] / 1e3 / std::max(1u, nev),
+                u64[8] / 1e3 / std::max(1u, nev), u64[9] / 1e3 / std::max(1u, nev));
+    if (getenv("DABS_ASYNC_PHASES"))
+        fprintf(stderr, "async CTA time: batches %.3f of lifetime; mean lifetime %.3f ms (kernel %.3f ms)\n",
+                (double)u64[10] / std::max(1ull, u64[11]), u64[11] / 1e6 / c->slots, (double)c->batch_ms);
+    return dabs_best(c, best_x, best_e);
+}
+
+extern "C" dabs_status dabs_async_lock_ns(const dabs_ctx* c, uint64_t* wait_ns, uint64_t* hold_ns)
+{
+    if (!c || !wait_ns || !hold_ns) return fail(DABS_E_ARG, "NULL argument");
+    *wait_ns = c->a_wait_ns;
+    *hold_ns = c->a_hold_ns;
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_async_log(const dabs_ctx* c, uint32_t* log, int64_t cap, int64_t* len)
+{
+    if (!c || !len) return fail(DABS_E_ARG, "NULL argument");
+    const int64_t m = (int64_t)c->a_log_h.size();
+    *len = m;
+    if (log && cap > 0) memcpy(log, c->a_log_h.data(), 4 * (size_t)std::min(cap, m));
+    return DABS_OK;
 }
 
 extern "C" dabs_status dabs_best(const dabs_ctx* c, uint8_t* best_x, int64_t* best_e)

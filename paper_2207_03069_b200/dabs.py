@@ -34,7 +34,7 @@ class dabs_config(C.Structure):
         ("slots_per_pool", C.c_uint32), ("target_energy", C.c_int64), ("time_limit_ns", C.c_uint64),
         ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
         ("cuda_stream", C.c_void_p), ("exchange", EXCHANGE_FN), ("alloc", ALLOC_FN), ("free", FREE_FN),
-        ("user", C.c_void_p), ("restart_gens", C.c_uint32), ("reserved", C.c_uint32),
+        ("user", C.c_void_p), ("restart_gens", C.c_uint32), ("flags", C.c_uint32),
     ]
 
 
@@ -56,6 +56,7 @@ class dabs_stats(C.Structure):
 EXPORTS = ["dabs_config_default", "dabs_create", "dabs_create_csr", "dabs_reset", "dabs_generation", "dabs_run",
            "dabs_best", "dabs_energy", "dabs_get_stats", "dabs_debug_batch", "dabs_read_slot", "dabs_read_pool",
            "dabs_read_packet", "dabs_read_stats_pool", "dabs_trace_enable", "dabs_trace_read",
+           "dabs_run_async", "dabs_async_log", "dabs_async_lock_ns",
            "dabs_last_error", "dabs_destroy"]
 
 _lib = None
@@ -87,6 +88,12 @@ def load(path: str = LIB_PATH):
     L.dabs_generation.restype = st
     L.dabs_run.argtypes = [P, u64, u64, P, P]
     L.dabs_run.restype = st
+    L.dabs_run_async.argtypes = [P, u64, u64, P, P]
+    L.dabs_run_async.restype = st
+    L.dabs_async_log.argtypes = [P, P, i64, P]
+    L.dabs_async_log.restype = st
+    L.dabs_async_lock_ns.argtypes = [P, P, P]
+    L.dabs_async_lock_ns.restype = st
     L.dabs_best.argtypes = [P, P, P]
     L.dabs_best.restype = st
     L.dabs_energy.argtypes = [P, P, P]
@@ -139,7 +146,8 @@ class Solver:
                  tabu: int = 8, cap: int = 100, eps_ppm: int = 50000, genop_mask: int = 0xFF, algo_mask: int = 0x1F,
                  restart_gens: int = 0,
                  pools: int = 1, slots: int = 0, target: int | None = None, time_limit_ns: int = 0,
-                 rank: int = 0, world: int = 1, device: int = -1, stream=None, exchange=None):
+                 rank: int = 0, world: int = 1, device: int = -1, stream=None, exchange=None,
+                 one_wave: bool = False):
         L = load()
         if csr is None:
             W = np.ascontiguousarray(W, dtype=np.int16)
@@ -158,6 +166,7 @@ class Solver:
         cfg.eps_ppm, cfg.genop_mask, cfg.algo_mask = eps_ppm, genop_mask, algo_mask
         cfg.pools_per_gpu, cfg.slots_per_pool = pools, slots
         cfg.restart_gens = restart_gens
+        cfg.flags = 1 if one_wave else 0
         cfg.target_energy = INT64_MIN if target is None else int(target)
         cfg.time_limit_ns = time_limit_ns
         cfg.rank, cfg.world, cfg.device = rank, world, device
@@ -213,6 +222,27 @@ class Solver:
         e = np.zeros(1, np.int64)
         _check(load().dabs_run(self.h, seed, flip_budget, _p(x), _p(e)))
         return int(e[0]), x
+
+    def run_async(self, seed: int, flip_budget: int):
+        """Asynchronous schedule (dabs_run_async): one persistent kernel."""
+        x = np.zeros(self.n, np.uint8)
+        e = np.zeros(1, np.int64)
+        _check(load().dabs_run_async(self.h, seed, flip_budget, _p(x), _p(e)))
+        return int(e[0]), x
+
+    def async_log(self) -> np.ndarray:
+        m = np.zeros(1, np.int64)
+        _check(load().dabs_async_log(self.h, None, 0, _p(m)))
+        out = np.zeros(int(m[0]), np.uint32)
+        if out.size:
+            _check(load().dabs_async_log(self.h, _p(out), out.size, _p(m)))
+        return out
+
+    def async_lock_ns(self):
+        w = np.zeros(1, np.uint64)
+        h = np.zeros(1, np.uint64)
+        _check(load().dabs_async_lock_ns(self.h, _p(w), _p(h)))
+        return int(w[0]), int(h[0])
 
     def best(self):
         x = np.zeros(self.n, np.uint8)

@@ -1,0 +1,103 @@
+"""GPU parity of the asynchronous schedule (R-29):
+dabs_run_async (one persistent kernel, pool lock, event log) vs the CPU
+oracle's replay of the device's own event log.  The log fixes only the ORDER
+of the merges; every batch, merge, seed, statistic and the run best are then
+recomputed by the oracle and must agree bit-exactly.
+"""
+import numpy as np
+import pytest
+
+from test_gpu_parity import compare_world, rand_upper
+
+pytestmark = pytest.mark.gpu
+SEEDED = 1 << 31
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2207_03069_b200 import build, dabs
+    build.build()
+    return dabs
+
+
+def check_log(log, slots):
+    s = log & 0x7FFFFFFF
+    assert s.max() < slots
+    last = {}
+    for e, v in enumerate(log):
+        last[int(v & 0x7FFFFFFF)] = e
+    assert sorted(last) == list(range(slots)), "every slot merges at least once"
+    for sl, e in last.items():
+        assert not (log[e] & SEEDED), "a slot's last event seeds nothing"
+
+
+def run_pair(orc, lib, U, P, S, seed, budget, one_wave=False, **kw):
+    solver = lib.Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=16, one_wave=one_wave, **kw)
+    Eg, Xg = solver.run_async(seed, budget)
+    log = solver.async_log()
+    check_log(log, solver.slots)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=solver.slots // P, cap=16,
+                     **{k: v for k, v in kw.items() if k in ("genop_mask", "algo_mask")})
+    w = orc.World(U, cfg)
+    w.reset(seed)
+    w.async_replay(log)
+    compare_world(orc, solver, w, P, 1)
+    Eo, Xo, rec = w.best()
+    assert Eg == Eo
+    np.testing.assert_array_equal(Xg, Xo)
+    st = solver.stats()
+    assert st.total_flips == w.total_flips
+    assert (st.best_algo, st.best_genop, st.best_generation, st.best_slot) == (
+        rec["algo"], rec["genop"], rec["gen"], rec["slot"])
+    assert st.generations == len(log)
+    return solver, log, st
+
+
+@pytest.mark.parametrize("n,P,S", [(40, 1, 3), (300, 3, 5), (1024, 2, 4), (2100, 2, 3), (5000, 2, 2)])
+def test_async_parity(orc, lib, n, P, S):
+    rng = np.random.default_rng(n + 1)
+    U = rand_upper(rng, n, -200, 200)
+    B = n   # b = 1
+    solver, log, st = run_pair(orc, lib, U, P, S, seed=4242, budget=6 * P * S * B)
+    assert st.total_flips >= 6 * P * S * B
+    # the stop rule: seeding ends at the first merge that reaches the budget
+    assert len(log) > P * S
+
+
+def test_async_parity_one_wave_warp_tier(orc, lib):
+    """Every resident warp-tier search of the GPU as a persistent CTA
+    (DABS_FLAG_ONE_WAVE), several pools, real lock contention."""
+    n = 160
+    U = rand_upper(np.random.default_rng(3), n, -50, 50)
+    solver, log, st = run_pair(orc, lib, U, P=4, S=0, seed=9, budget=1, one_wave=True)
+    assert solver.slots >= 148
+    assert len(log) == solver.slots   # budget 1: every slot stops after its first batch
+
+
+def test_async_parity_one_wave_many_batches(orc, lib):
+    n = 96
+    U = rand_upper(np.random.default_rng(5), n, -30, 30)
+    solver, log, st = run_pair(orc, lib, U, P=2, S=0, seed=17, budget=0, one_wave=True)
+    solver2, log2, st2 = run_pair(orc, lib, U, P=2, S=0, seed=17, budget=4 * solver.slots * 10 * n,
+                                  one_wave=True)
+    assert len(log2) >= 3 * solver2.slots
+
+
+def test_async_target_stop(orc, lib):
+    """The run stops seeding once the best reaches the target (K16 optimum)."""
+    import itertools
+    from paper_2207_03069_b200 import workloads as wl
+    U = wl.random_dense(16, 1)
+    X = np.array(list(itertools.product([0, 1], repeat=16)), np.int64)
+    opt = int(np.einsum("bi,ij,bj->b", X, U.astype(np.int64), X).min())
+    solver, log, st = run_pair(orc, lib, U, P=1, S=4, seed=3, budget=1 << 40, target=opt)
+    assert st.best_energy == opt
+
+
+def test_async_rejects(lib):
+    U = rand_upper(np.random.default_rng(1), 50, -5, 5)
+    s = lib.Solver(U, pools=1, slots=2, restart_gens=3)
+    with pytest.raises(lib.DabsError):
+        s.run_async(1, 1000)
