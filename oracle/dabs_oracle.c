@@ -536,6 +536,8 @@ typedef struct {
     uint64_t gen_flips;
     int checked;
     int err;
+    /* asynchronous schedule (R-29): per-slot batch index, finished, XREAD pending */
+    uint32_t* a_k; uint8_t* a_done; uint8_t* a_pending; int64_t a_events;
 } world_t;
 
 static void pool_alloc(pool_t* p, int cap, int n)
@@ -612,6 +614,7 @@ void orc_world_free(void* vw)
     free(w->sx); free(w->sdelta); free(w->sE); free(w->sring);
     free(w->D); free(w->palgo); free(w->pgenop); free(w->rbest); free(w->rE); free(w->rflips);
     free(w->dispatch); free(w->inserted); free(w->best_X);
+    free(w->a_k); free(w->a_done); free(w->a_pending);
     free(w);
 }
 
@@ -730,6 +733,47 @@ static void ga_seed_g(world_t* w, int s, uint32_t gen, int live_ring)
 
 static void ga_seed(world_t* w, int s) { ga_seed_g(w, s, w->gen, 0); }
 
+/* Asynchronous schedule, R-29: an Xrossover packet whose partner is another
+   pool is built in two steps.  At the merge event only the bits the mask
+   takes from the own parent A are set (D = A where m0, 0 elsewhere; i.e.
+   orc_build_target with an all-zero B); the slot's next XREAD event fills
+   the others from the partner pool's rank-r2 row as the pool is then.
+   Returns 1 if the packet is pending. */
+static int ga_seed_async(world_t* w, int s, uint32_t gen)
+{
+    int p = s / w->S;
+    int pn = (p + 1) % w->P;
+    if (pn == p) { ga_seed_g(w, s, gen, 1); return 0; }
+    /* same draws as ga_seed_g; the partner row is replaced by zeros */
+    pool_t saved = w->pools[pn];
+    pool_t zero;
+    pool_alloc(&zero, w->cap, w->n);   /* calloc: all-zero rows */
+    w->pools[pn] = zero;
+    ga_seed_g(w, s, gen, 1);
+    w->pools[pn] = saved;
+    pool_free(&zero);
+    return w->pgenop[s] == GEN_XROSSOVER;
+}
+
+/* the XREAD step: D[k] = partner row r2, bit k, wherever mask word bit m0 = 0 */
+static void xread_async(world_t* w, int s, uint32_t gen)
+{
+    int n = w->n;
+    int p = s / w->S;
+    int pn = (p + 1) % w->P;
+    uint32_t gs = (uint32_t)(w->rank * w->P * w->S + s);
+    uint32_t b[4];
+    rng4(w->seed, PUR_GA_PARENT, 0, gs, gen, 0, b);
+    uint32_t r2 = rank_pick(b[1], (uint32_t)w->cap);
+    const uint8_t* B = w->pools[pn].X + (size_t)r2 * n;
+    uint8_t* D = w->D + (size_t)s * n;
+    for (int k = 0; k < n; k++) {
+        uint32_t m[4];
+        rng4(w->seed, PUR_GA_MASK, (uint32_t)(k / 32), gs, gen, 0, m);
+        if (!((m[0] >> (k % 32)) & 1)) D[k] = B[k];
+    }
+}
+
 /* merge one pool (R-18): stable sort of old ++ new by (E, seq),
    drop results equal in (E, X) to an earlier finite entry, keep `cap`. */
 typedef struct { int64_t E; uint64_t seq; int src; /* <0: old row -(r+1); >=0: slot */ } cand_t;
@@ -837,49 +881,98 @@ int orc_world_generation_local(void* vw)
    updated on strict improvement; then, if `seeded`, packet k+1 is drawn from
    the pools as they are after this merge, with the last pool's Xrossover
    partner = local pool 0, live (R-29).  Single rank only.
+   An Xrossover packet whose partner is another pool is completed by the
+   slot's XREAD event (log entry s | 1<<30), which reads the partner pool as
+   it is at that point of the log (ga_seed_async / xread_async above).
    Returns 0, or 20 (bad slot), 21 (event after the slot's last batch),
-   22 (a slot without a final unseeded event), or a batch error. */
-int orc_world_async_replay(void* vw, const uint32_t* log, int64_t len)
+   22 (a slot without a final unseeded event), 24 (a batch or XREAD out of
+   turn), or a batch error. */
+static void async_free(world_t* w)
+{
+    free(w->a_k); free(w->a_done); free(w->a_pending);
+    w->a_k = NULL; w->a_done = NULL; w->a_pending = NULL;
+}
+
+/* start of an asynchronous run (after orc_world_reset): packet 0 of every slot */
+int orc_world_async_begin(void* vw)
+{
+    world_t* w = (world_t*)vw;
+    int ns = w->P * w->S;
+    if (w->world != 1) return 23;
+    async_free(w);
+    w->a_k = (uint32_t*)calloc(ns, sizeof(uint32_t));
+    w->a_done = (uint8_t*)calloc(ns, 1);
+    w->a_pending = (uint8_t*)calloc(ns, 1);
+    w->a_events = 0;
+    for (int s = 0; s < ns; s++) ga_seed_g(w, s, 0, 1);
+    return 0;
+}
+
+/* one log entry; returns 0 / 1 (the slot's packet now waits for its XREAD)
+   or -error */
+int orc_world_async_event(void* vw, uint32_t entry)
 {
     world_t* w = (world_t*)vw;
     int n = w->n, ns = w->P * w->S;
-    if (w->world != 1) return 23;
-    uint32_t* k = (uint32_t*)calloc(ns, sizeof(uint32_t));
-    uint8_t* done = (uint8_t*)calloc(ns, 1);
-    int err = 0;
-    for (int s = 0; s < ns; s++) ga_seed_g(w, s, 0, 1);
-    for (int64_t e = 0; e < len && !err; e++) {
-        int s = (int)(log[e] & 0x7FFFFFFFu);
-        int seeded = (int)(log[e] >> 31);
-        if (s >= ns) { err = 20; break; }
-        if (done[s]) { err = 21; break; }
-        uint32_t gs = (uint32_t)s;
-        err = orc_batch(w->U, n, w->T, w->B, w->tabu,
+    int s = (int)(entry & 0x3FFFFFFFu);
+    int seeded = (int)(entry >> 31);
+    int xread = (int)((entry >> 30) & 1u);
+    int64_t e = w->a_events;
+    if (!w->a_k) return -25;
+    if (s >= ns) return -20;
+    if (w->a_done[s]) return -21;
+    if (xread != w->a_pending[s]) return -24;
+    w->a_events++;
+    if (xread) {
+        xread_async(w, s, w->a_k[s]);
+        w->a_pending[s] = 0;
+        return 0;
+    }
+    uint32_t gs = (uint32_t)s;
+    int err = orc_batch(w->U, n, w->T, w->B, w->tabu,
                         w->sx + (size_t)s * n, w->sdelta + (size_t)s * n, &w->sE[s],
                         w->sring + (size_t)s * ORC_TABU_MAX,
-                        w->D + (size_t)s * n, w->palgo[s], w->seed, gs, k[s],
+                        w->D + (size_t)s * n, w->palgo[s], w->seed, gs, w->a_k[s],
                         w->rbest + (size_t)s * n, &w->rE[s], &w->rflips[s],
                         NULL, NULL, NULL, 0, w->checked);
-        if (err) break;
-        w->total_flips += (uint64_t)w->rflips[s];
-        uint64_t seq = ((uint64_t)(e + 1) << 32) | gs;
-        merge_results(w, s / w->S, &s, &seq, 1);
-        if (w->rE[s] < w->best_E) {
-            w->best_E = w->rE[s];
-            memcpy(w->best_X, w->rbest + (size_t)s * n, n);
-            w->best_algo = w->palgo[s]; w->best_genop = w->pgenop[s];
-            w->best_gen = e; w->best_slot = gs;
-        }
-        if (seeded) {
-            k[s]++;
-            ga_seed_g(w, s, k[s], 1);
-        } else {
-            done[s] = 1;
-        }
+    if (err) return -err;
+    w->total_flips += (uint64_t)w->rflips[s];
+    uint64_t seq = ((uint64_t)(e + 1) << 32) | gs;
+    merge_results(w, s / w->S, &s, &seq, 1);
+    if (w->rE[s] < w->best_E) {
+        w->best_E = w->rE[s];
+        memcpy(w->best_X, w->rbest + (size_t)s * n, n);
+        w->best_algo = w->palgo[s]; w->best_genop = w->pgenop[s];
+        w->best_gen = e; w->best_slot = gs;
     }
-    for (int s = 0; s < ns && !err; s++) if (!done[s]) err = 22;
-    free(k);
-    free(done);
+    if (seeded) {
+        w->a_k[s]++;
+        w->a_pending[s] = (uint8_t)ga_seed_async(w, s, w->a_k[s]);
+        return w->a_pending[s];
+    }
+    w->a_done[s] = 1;
+    return 0;
+}
+
+/* end of the log: every slot has merged its final batch */
+int orc_world_async_end(void* vw)
+{
+    world_t* w = (world_t*)vw;
+    int ns = w->P * w->S;
+    if (!w->a_k) return 25;
+    for (int s = 0; s < ns; s++) if (!w->a_done[s]) return 22;
+    return 0;
+}
+
+int orc_world_async_replay(void* vw, const uint32_t* log, int64_t len)
+{
+    world_t* w = (world_t*)vw;
+    int err = orc_world_async_begin(vw);
+    for (int64_t e = 0; e < len && !err; e++) {
+        int r = orc_world_async_event(vw, log[e]);
+        if (r < 0) err = -r;
+    }
+    if (!err) err = orc_world_async_end(vw);
     if (err) w->err = err;
     return err;
 }

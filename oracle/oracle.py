@@ -92,6 +92,12 @@ def lib():
         L.orc_world_get_best.argtypes = [P, P, P, P]
         L.orc_world_async_replay.argtypes = [P, P, C.c_int64]
         L.orc_world_async_replay.restype = C.c_int
+        L.orc_world_async_begin.argtypes = [P]
+        L.orc_world_async_begin.restype = C.c_int
+        L.orc_world_async_event.argtypes = [P, u32]
+        L.orc_world_async_event.restype = C.c_int
+        L.orc_world_async_end.argtypes = [P]
+        L.orc_world_async_end.restype = C.c_int
         L.orc_lowbias32.argtypes = [u32]
         L.orc_lowbias32.restype = u32
         L.orc_rank_pick.argtypes = [u32, u32]
@@ -319,6 +325,24 @@ class World:
         err = lib().orc_world_async_replay(self.h, _p(lg), int(lg.size))
         if err:
             raise RuntimeError(f"oracle async replay error {err}")
+
+    def async_begin(self) -> None:
+        err = lib().orc_world_async_begin(self.h)
+        if err:
+            raise RuntimeError(f"oracle async begin error {err}")
+
+    def async_event(self, entry: int) -> int:
+        """One log entry (slot | seeded<<31 | xread<<30); returns 1 when the
+        slot's new packet waits for its XREAD event (R-29)."""
+        r = lib().orc_world_async_event(self.h, int(entry))
+        if r < 0:
+            raise RuntimeError(f"oracle async event error {-r}")
+        return r
+
+    def async_end(self) -> None:
+        err = lib().orc_world_async_end(self.h)
+        if err:
+            raise RuntimeError(f"oracle async end error {err}")
 
     def export(self) -> np.ndarray:
         buf = np.zeros(self.payload_bytes, np.uint8)
