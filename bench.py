@@ -350,8 +350,11 @@ def main():
     # search, no generation barrier -- for the same flips as the timed steps.
     # Kernel time by CUDA events on the library's stream (batch_ms_last).
     if world == 1 and not args.no_async and solver.threads * 1 <= 512 and n <= 32768:
+        # pools: the paper's ~216 searches per pool, one wave of
+        # resident searches (a quarter of the generation schedule's four waves)
+        a_pools = max(1, round(solver.slots / 4 / 216))
         sa = Solver(None if csr else U, csr=csr, s_milli=meta["s_milli"], b_milli=meta["b_milli"],
-                    pools=meta.get("pools", 1), one_wave=True, device=torch.cuda.current_device(),
+                    pools=a_pools, one_wave=True, device=torch.cuda.current_device(),
                     stream=stream.cuda_stream)
         budget = int(sum(local_flips))
         sa.run_async(args.seed, max(1, budget // 4))   # warm-up
@@ -369,9 +372,10 @@ def main():
             "lock_busy_frac": hold_ns / 1e6 / max(1e-9, sta.batch_ms_last),
             "value": sta.total_flips / (sta.batch_ms_last / 1e3), "unit": UNIT,
             "wall_value": sta.total_flips / wall, "flips": int(sta.total_flips),
-            "merge_events": int(sta.generations), "slots": int(sa.slots), "kernel_ms": float(sta.batch_ms_last),
+            "merge_events": int(sta.generations), "slots": int(sa.slots), "pools": a_pools,
+            "kernel_ms": float(sta.batch_ms_last),
             "vs_generation_schedule": (sta.total_flips / (sta.batch_ms_last / 1e3)) / value,
-            "what": "dabs_run_async: persistent kernel, one CTA per resident search, device-side pool lock, "
+            "what": "dabs_run_async: persistent kernel, one CTA per resident search, per-pool ticket locks, "
                     "merge/seed per batch (no generation barrier); value = flips / kernel time"}
         sa.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -126,14 +126,13 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             mpre[j] = lane + 32 * j < nwp ? rng4(g.seed, PUR_GA_MASK, (uint32_t)(lane + 32 * j), gs, gen1, 0)
                                          : make_uint4(0, 0, 0, 0);
 
-        // Per-pool ticket locks.  An event holds its own pool's lock and, when its
-        // next packet is an Xrossover, its partner's; it takes its event index
-        // only once it holds every lock it needs.  Two events that touch a
-        // common pool are then ordered the same way by that pool's lock and by
-        // their indices, so replaying the log in index order reproduces every
-        // pool's history.  Locks are taken in ascending pool order (no
-        // deadlock): the last pool, whose partner is pool 0, releases its lock
-        // and starts over with pool 0 first when it finds it needs it.
+        // Per-pool ticket locks.  Every event holds exactly one pool's lock and
+        // takes its event index under it.  Two events that touch the same pool
+        // are then ordered the same way by that pool's lock and by their
+        // indices, so replaying the log in index order reproduces every pool's
+        // history.  An Xrossover packet whose partner is another pool is
+        // finished by a second event (XREAD) under the partner's lock after
+        // this one is released (R-29): no lock is ever held while waiting.
         auto lock = [&](int q) {
             const uint32_t tk = atomicAdd(a.ticket + 32 * q, 1u);
             // poll with relaxed loads (an acquire load would invalidate the SM's L1
@@ -150,19 +149,15 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         auto unlock = [&](int q, uint32_t tk) {
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.serving + 32 * q), "r"(tk + 1) : "memory");
         };
-        uint32_t tk_own = 0, tk_succ = 0;
-        bool hold_succ = false;
+        uint32_t tk_own = 0;
         const unsigned long long t_req = globaltimer();
         unsigned long long t_acq = 0, t_B = 0, t_D = 0;
         int64_t bE = 0;
         int32_t bev = 0;
         int stop0 = 0, pos = 0, genop = 0;
         bool ins = false;
-        for (;;) {
-            if (lane == 0) {
-                if (hold_succ) tk_succ = lock(pn);
-                tk_own = lock(p);
-            }
+        {
+            if (lane == 0) tk_own = lock(p);
             __syncwarp();
             t_acq = globaltimer();
             // round A
@@ -226,15 +221,8 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
                 const uint32_t q = (ins && pg > (uint32_t)pos) ? pg - 1 : pg;
                 genop = (int)__ldcg(pool.genop + ord_s[q]);
             }
-            if (genop != GEN_XROSSOVER || pn == p || hold_succ) break;
-            if (pn > p) {
-                if (lane == 0) tk_succ = lock(pn);
-                hold_succ = true;
-                break;
-            }
-            if (lane == 0) unlock(p, tk_own);   // partner first: start over
-            hold_succ = true;
         }
+        const bool xpend = genop == GEN_XROSSOVER && pn != p;   // finished by an XREAD event
         uint32_t e = 0;
         unsigned long long fl = 0;
         if (lane == 0) {
@@ -244,7 +232,6 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         e = __shfl_sync(0xffffffffu, e, 0);
         fl = __shfl_sync(0xffffffffu, fl, 0);
         const unsigned long long t0 = a.time_limit_ns ? __ldcg(a.t0) : 0ull;
-        const int32_t so2 = (genop == GEN_XROSSOVER && pn != p) ? __ldcg(a.ord + (size_t)pn * cap + r2) : 0;
         const int32_t victim = ord_s[cap - 1];
         if (ins) {
             for (int w = lane; w < nwp; w += 32) __stcg(pool.X + (size_t)victim * nwp + w, Xr[w]);
@@ -300,7 +287,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         const int64_t bE2 = Er < bE ? Er : bE;
         const bool stop = stop0 != 0 || fl >= a.budget || (a.target != INT64_MIN && bE2 <= a.target) ||
                           (a.time_limit_ns && now - t0 >= a.time_limit_ns) ||
-                          (uint64_t)e + 1 + (uint64_t)a.slots >= (uint64_t)a.log_cap;
+                          (uint64_t)e + 1 + 2 * (uint64_t)a.slots >= (uint64_t)a.log_cap;
         const bool seeded = !stop;
         if (lane == 0) {
             if (stop) __stcg(a.stop, 1);
@@ -313,14 +300,14 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             const bool newA = ins && r1 == (uint32_t)pos, newB = ins && r2 == (uint32_t)pos, new0 = ins && pos == 0;
             const uint32_t* A = newA ? Xr : pool.X + (size_t)ord_n[r1] * nwp;
             const uint32_t* Bo = newB ? Xr : pool.X + (size_t)ord_n[r2] * nwp;
-            const uint32_t* Bs = (pn == p) ? Bo : succ.X + (size_t)so2 * nwp;
+            const uint32_t* Bs = Bo;   // Xrossover: own pool (P = 1); across pools the XREAD fills it
             const uint32_t* B0 = new0 ? Xr : pool.X + (size_t)ord_n[0] * nwp;
             const int algo = a_rand ? g.algs[pick_u(ga.w, (uint32_t)g.n_alg)]
                                     : (ins && pa == (uint32_t)pos ? (int)alg : (int)__ldcg(pool.algo + ord_n[pa]));
             uint32_t* Dout = a.D + (size_t)s * nwp;
             auto emit = [&](int w, const uint4 m) {
                 const uint32_t va = __ldcg(A + w), vbo = __ldcg(Bo + w), vbs = __ldcg(Bs + w), v0 = __ldcg(B0 + w);
-                const uint32_t vb = genop == GEN_XROSSOVER ? vbs : vbo;
+                const uint32_t vb = genop == GEN_XROSSOVER ? (xpend ? 0u : vbs) : vbo;
                 const uint32_t p8 = m.x & m.y & m.z;
                 uint32_t v;
                 switch (genop) {
@@ -361,12 +348,33 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         const unsigned long long t_R = globaltimer();
         if (lane == 0) {
             unlock(p, tk_own);
-            if (hold_succ) unlock(pn, tk_succ);
             sh_seeded = seeded ? 1 : 0;
             const unsigned long long t_rel = globaltimer();
             atomicAdd(a.lock_ns, t_acq - t_req);
             atomicAdd(a.lock_ns + 2, t_B - t_acq); atomicAdd(a.lock_ns + 3, t_D - t_B); atomicAdd(a.lock_ns + 4, t_G - t_D); atomicAdd(a.lock_ns + 5, t_R - t_G); atomicAdd(a.lock_ns + 6, t_rel - t_R);
             atomicAdd(a.lock_ns + 1, t_rel - t_acq);
+        }
+        // XREAD (R-29): the partner pool's rank-r2 row fills the bits the mask
+        // does not take from the own parent
+        if (seeded && xpend) {
+            uint32_t tk = 0, e2 = 0;
+            if (lane == 0) {
+                tk = lock(pn);
+                e2 = atomicAdd(a.evcount, 1u);
+            }
+            __syncwarp();
+            const int32_t o2 = __ldcg(a.ord + (size_t)pn * cap + r2);
+            const uint32_t* Bx = succ.X + (size_t)o2 * nwp;
+            uint32_t* Dout = a.D + (size_t)s * nwp;
+            for (int w = lane; w < nwp; w += 32) {
+                const uint4 m = w < 64 ? (w < 32 ? mpre[0] : mpre[1]) : rng4(g.seed, PUR_GA_MASK, (uint32_t)w, gs, gen1, 0);
+                Dout[w] |= __ldcg(Bx + w) & ~m.x;   // bits >= n: zero in every pool row
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __stcg(a.log + e2, (uint32_t)s | 0x40000000u);
+                unlock(pn, tk);
+            }
         }
     }
     __syncthreads();

@@ -11,6 +11,8 @@ from test_gpu_parity import compare_world, rand_upper
 
 pytestmark = pytest.mark.gpu
 SEEDED = 1 << 31
+XREAD = 1 << 30
+SLOT = (1 << 30) - 1
 
 
 @pytest.fixture(scope="module")
@@ -23,14 +25,14 @@ def lib():
 
 
 def check_log(log, slots):
-    s = log & 0x7FFFFFFF
+    s = log & SLOT
     assert s.max() < slots
     last = {}
     for e, v in enumerate(log):
-        last[int(v & 0x7FFFFFFF)] = e
+        last[int(v & SLOT)] = e
     assert sorted(last) == list(range(slots)), "every slot merges at least once"
     for sl, e in last.items():
-        assert not (log[e] & SEEDED), "a slot's last event seeds nothing"
+        assert not (log[e] & (SEEDED | XREAD)), "a slot's last event is a merge that seeds nothing"
 
 
 def run_pair(orc, lib, U, P, S, seed, budget, one_wave=False, **kw):
@@ -55,7 +57,7 @@ def run_pair(orc, lib, U, P, S, seed, budget, one_wave=False, **kw):
     return solver, log, st
 
 
-@pytest.mark.parametrize("n,P,S", [(40, 1, 3), (300, 3, 5), (1024, 2, 4), (2100, 2, 3), (5000, 2, 2)])
+@pytest.mark.parametrize("n,P,S", [(40, 1, 3), (300, 3, 5), (1024, 2, 4), (2100, 2, 3), (5000, 2, 2), (700, 4, 3)])
 def test_async_parity(orc, lib, n, P, S):
     rng = np.random.default_rng(n + 1)
     U = rand_upper(rng, n, -200, 200)
@@ -64,6 +66,8 @@ def test_async_parity(orc, lib, n, P, S):
     assert st.total_flips >= 6 * P * S * B
     # the stop rule: seeding ends at the first merge that reaches the budget
     assert len(log) > P * S
+    if P * S >= 12:
+        assert (log & XREAD).any(), "Xrossover across pools exercised"
 
 
 def test_async_parity_one_wave_warp_tier(orc, lib):

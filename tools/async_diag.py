@@ -28,7 +28,7 @@ def one(n, P, S, mult, seed=4242, mask=0xFF):
     print(f"n={n} P={P} S={S} mult={mult} mask={mask:#x} events={len(log)} pools_bad={bad} slots_bad={slots_bad}",
           flush=True)
     if bad or slots_bad:
-        print("  log:", [(int(v) & 0x7fffffff, int(v) >> 31) for v in log[:60]])
+        print("  log:", [(int(v) & 0x3fffffff, (int(v) >> 30)) for v in log[:60]])
 
 
 for args in [(300, 1, 5, 6), (300, 3, 1, 6), (300, 2, 1, 6), (300, 3, 5, 6), (300, 3, 5, 1), (300, 3, 5, 6, 4242, 0xFB),
