@@ -138,11 +138,13 @@ dabs_status dabs_run(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t
  * packet flow without a generation barrier).
  * dabs_reset(seed); packet 0 of every slot is seeded from the fresh pools;
  * then ONE persistent kernel, one CTA per slot, runs batch after batch: after
- * batch k a slot takes the rank's pool lock, merges its result into its pool
+ * batch k a slot takes its pool's lock, merges its result into its pool
  * (R-18 with one newcomer, seq = (event+1)<<32 | slot), updates the run best,
  * appends (slot | seeded<<31) to the event log and, unless the run is
- * stopping, seeds packet k+1 (Philox generation field = k+1) from the pools as
- * they are (the last pool's Xrossover partner is local pool 0, live).  The
+ * stopping, seeds packet k+1 (Philox generation field = k+1) from its pool as
+ * it is.  An Xrossover packet whose partner (local pool (p+1) mod P, live) is
+ * another pool is completed by a second event (XREAD) under the partner's
+ * lock, after the own lock is released: no lock is held while waiting.  The
  * run stops seeding once the merged flips >= flip_budget, best <=
  * target_energy, or the time limit has passed (device clock); every slot then
  * merges its running batch and exits.  Deterministic given the log: the CPU
@@ -151,13 +153,13 @@ dabs_status dabs_run(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t
  * resident capacity start only after the stop).  Requires world == 1, the CTA
  * tiers (n <= 32768), restart_gens == 0 and tracing off, else DABS_E_ARG.
  * Writes the best vector (n bytes, host) and energy; dabs_get_stats then
- * reports the run (generations = merge events, time_to_best_ns from the
+ * reports the run (generations = events, time_to_best_ns from the
  * kernel's start on the device clock, batch_ms_last = the kernel's time). */
 dabs_status dabs_run_async(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t* best_x_host,
                            int64_t* best_e);
 
-/* The last dabs_run_async's event log, in merge order: entry = local slot |
- * (1<<31 if a next packet was seeded).  Copies min(cap, len) entries to `log`
+/* The last dabs_run_async's event log, in event order: a merge is local slot
+ * | (1<<31 if a next packet was seeded); an XREAD is local slot | (1<<30).  Copies min(cap, len) entries to `log`
  * (host, caller-owned; may be NULL), *len = the number of events. */
 dabs_status dabs_async_log(const dabs_ctx* ctx, uint32_t* log, int64_t cap, int64_t* len);
 
