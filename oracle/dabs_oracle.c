@@ -140,6 +140,7 @@ typedef struct {
     int phase;
     /* checked mode: recompute E and Delta from scratch after every flip */
     int checked;
+    int jump;          /* jump-start (R-30): X <- D before the batch instead of Straight's flips */
     int err;
     int32_t* scratch;  /* n, for checked mode */
     uint8_t* scratch_x;
@@ -414,6 +415,15 @@ static void batch(search_t* s, const uint8_t* D, int algo)
     uint8_t* cand = (uint8_t*)malloc(n);
     s->ebest = ORC_E_INF;
     s->flips = 0;
+    if (s->jump) {
+        /* jump-start (P:498-500 read with SURVEY f4, R-30): the batch starts AT
+           the target: X = D, E = E(D) by Eq.(2), Delta by Eq.(3) from scratch;
+           no flips, no scans, the tabu ring untouched.  Straight then has
+           nothing to do. */
+        memcpy(s->x, D, n);
+        s->E = orc_energy(s->U, n, s->x);
+        orc_delta_closed(s->U, n, s->x, s->delta);
+    }
     straight(s, D);
     if (!s->err) greedy(s);
     int round = 0;
@@ -460,8 +470,16 @@ int orc_batch(const int16_t* U, int n, int T, int B, int tabu,
                              flips, tr_bit, tr_E, tr_phase, tr_cap, checked, 0);
 }
 
-/* Same as orc_batch, but stops after flip_limit flips (returns 4): a bounded
-   sample of a batch, used only to time the oracle (bench cpu_baseline). */
+/* orc_batch with the jump-start variant (jump = 1, R-30) and a flip limit
+   (> 0: stop after that many flips, returns 4; a bounded sample of a batch,
+   used only to time the oracle in bench cpu_baseline). */
+int orc_batch_ex(const int16_t* U, int n, int T, int B, int tabu,
+                 uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
+                 const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
+                 uint8_t* best, int64_t* ebest, int64_t* flips,
+                 int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked,
+                 int64_t flip_limit, int jump);
+
 int orc_batch_limited(const int16_t* U, int n, int T, int B, int tabu,
                       uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
                       const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
@@ -469,9 +487,21 @@ int orc_batch_limited(const int16_t* U, int n, int T, int B, int tabu,
                       int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked,
                       int64_t flip_limit)
 {
+    return orc_batch_ex(U, n, T, B, tabu, x, delta, E, ring, D, algo, seed, slot, gen, best, ebest, flips,
+                        tr_bit, tr_E, tr_phase, tr_cap, checked, flip_limit, 0);
+}
+
+int orc_batch_ex(const int16_t* U, int n, int T, int B, int tabu,
+                 uint8_t* x, int32_t* delta, int64_t* E, int32_t* ring,
+                 const uint8_t* D, int algo, uint64_t seed, uint32_t slot, uint32_t gen,
+                 uint8_t* best, int64_t* ebest, int64_t* flips,
+                 int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase, int64_t tr_cap, int checked,
+                 int64_t flip_limit, int jump)
+{
     search_t s;
     memset(&s, 0, sizeof s);
     s.flip_limit = flip_limit;
+    s.jump = jump;
     s.n = n; s.U = U; s.x = x; s.delta = delta; s.E = *E; s.ring = ring; s.tabu = tabu;
     s.best = best; s.T = T; s.B = B; s.seed = seed; s.slot = slot; s.gen = gen;
     s.tr_bit = tr_bit; s.tr_E = tr_E; s.tr_phase = tr_phase; s.tr_cap = tr_cap;
@@ -538,6 +568,7 @@ typedef struct {
     int err;
     /* asynchronous schedule (R-29): per-slot batch index, finished, XREAD pending */
     uint32_t* a_k; uint8_t* a_done; uint8_t* a_pending; int64_t a_events;
+    int jump;   /* jump-start batches (R-30) */
 } world_t;
 
 static void pool_alloc(pool_t* p, int cap, int n)
@@ -620,6 +651,7 @@ void orc_world_free(void* vw)
 
 void orc_world_set_checked(void* vw, int checked) { ((world_t*)vw)->checked = checked; }
 void orc_world_set_restart(void* vw, uint32_t gens) { ((world_t*)vw)->restart_gens = gens; }
+void orc_world_set_jump(void* vw, int jump) { ((world_t*)vw)->jump = jump; }
 uint32_t orc_world_restarts(void* vw) { return ((world_t*)vw)->restarts; }
 
 /* pools from Philox (counter generation `gen`), slots at X=0, E=0,
@@ -856,12 +888,12 @@ int orc_world_generation_local(void* vw)
     w->gen_flips = 0;
     for (int s = 0; s < ns; s++) {
         uint32_t gs = (uint32_t)(w->rank * ns + s);
-        int err = orc_batch(w->U, n, w->T, w->B, w->tabu,
-                            w->sx + (size_t)s * n, w->sdelta + (size_t)s * n, &w->sE[s],
-                            w->sring + (size_t)s * ORC_TABU_MAX,
-                            w->D + (size_t)s * n, w->palgo[s], w->seed, gs, w->gen,
-                            w->rbest + (size_t)s * n, &w->rE[s], &w->rflips[s],
-                            NULL, NULL, NULL, 0, w->checked);
+        int err = orc_batch_ex(w->U, n, w->T, w->B, w->tabu,
+                               w->sx + (size_t)s * n, w->sdelta + (size_t)s * n, &w->sE[s],
+                               w->sring + (size_t)s * ORC_TABU_MAX,
+                               w->D + (size_t)s * n, w->palgo[s], w->seed, gs, w->gen,
+                               w->rbest + (size_t)s * n, &w->rE[s], &w->rflips[s],
+                               NULL, NULL, NULL, 0, w->checked, 0, w->jump);
         if (err) { w->err = err; return err; }
         w->gen_flips += (uint64_t)w->rflips[s];
     }

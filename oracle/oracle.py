@@ -60,6 +60,8 @@ def lib():
         L.orc_batch.restype = C.c_int
         L.orc_batch_limited.argtypes = L.orc_batch.argtypes + [i64]
         L.orc_batch_limited.restype = C.c_int
+        L.orc_batch_ex.argtypes = L.orc_batch.argtypes + [i64, C.c_int]
+        L.orc_batch_ex.restype = C.c_int
         L.orc_step_flip.argtypes = [P, C.c_int, P, P, P, P, C.c_int]
         L.orc_world_new.argtypes = [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     u32, u32, u32, C.c_int, C.c_int, C.c_int, C.c_int]
@@ -67,6 +69,7 @@ def lib():
         L.orc_world_free.argtypes = [P]
         L.orc_world_set_checked.argtypes = [P, C.c_int]
         L.orc_world_set_restart.argtypes = [P, u32]
+        L.orc_world_set_jump.argtypes = [P, C.c_int]
         L.orc_world_restarts.argtypes = [P]
         L.orc_world_restarts.restype = u32
         L.orc_world_reset.argtypes = [P, u64]
@@ -191,8 +194,9 @@ class BatchResult:
 
 def batch(U: np.ndarray, state: SlotState, D: np.ndarray, algo: int, *, T: int, B: int,
           tabu: int = 8, seed: int = 0, slot: int = 0, gen: int = 0,
-          trace_cap: int = 0, checked: bool = False) -> BatchResult:
-    """Run one batch search in place on ``state``."""
+          trace_cap: int = 0, checked: bool = False, jump: bool = False) -> BatchResult:
+    """Run one batch search in place on ``state``; jump = the
+    jump-start variant (R-30)."""
     U = np.ascontiguousarray(U, dtype=np.int16)
     n = U.shape[0]
     D = np.ascontiguousarray(D, dtype=np.uint8)
@@ -208,9 +212,9 @@ def batch(U: np.ndarray, state: SlotState, D: np.ndarray, algo: int, *, T: int, 
     else:
         tb = te = tp = None
         tptr = (None, None, None)
-    err = lib().orc_batch(_p(U), n, T, B, tabu, _p(state.x), _p(state.delta), _p(E), _p(state.ring),
-                          _p(D), algo, seed, slot, gen, _p(best), _p(ebest), _p(flips),
-                          *tptr, trace_cap, int(checked))
+    err = lib().orc_batch_ex(_p(U), n, T, B, tabu, _p(state.x), _p(state.delta), _p(E), _p(state.ring),
+                             _p(D), algo, seed, slot, gen, _p(best), _p(ebest), _p(flips),
+                             *tptr, trace_cap, int(checked), 0, int(jump))
     if err:
         raise RuntimeError(f"oracle batch error {err}")
     state.E = int(E[0])
@@ -263,6 +267,7 @@ class Config:
     pools: int = 1          # pools per rank
     slots: int = 1          # slots per pool
     restart_gens: int = 0   # restart-on-merge after this many stalled generations (R-28); 0 = off
+    jump: bool = False      # jump-start batches (R-30): X <- D instead of Straight
 
 
 class World:
@@ -279,6 +284,7 @@ class World:
                                  cfg.pools, cfg.slots, rank, world)
         L.orc_world_set_checked(self.h, int(checked))
         L.orc_world_set_restart(self.h, int(cfg.restart_gens))
+        L.orc_world_set_jump(self.h, int(cfg.jump))
         self.payload_bytes = int(L.orc_world_payload_bytes(self.h))
 
     def __del__(self):
