@@ -19,6 +19,8 @@
 #include "batch_kernel.cuh"
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
+#include "jump_kernels.cuh"
+#include <cublas_v2.h>
 
 using namespace dabs;
 
@@ -101,7 +103,13 @@ struct dabs_ctx {
     // asynchronous schedule
     uint32_t* a_lock = nullptr;      // tickets [P*32], serving [P*32], evcount, stop, best lock (own lines)
     uint64_t* a_hash = nullptr;      // [P][cap]
-    uint64_t a_wait_ns = 0, a_hold_ns = 0;   // last async run: summed pool-lock wait / hold (device clock)
+    uint64_t a_wait_ns = 0, a_hold_ns = 0;
+    // jump-start
+    bool jump = false;
+    cublasHandle_t cub = nullptr;
+    __half *Whi = nullptr, *Wlo = nullptr, *Dx = nullptr;
+    float *Chi = nullptr, *Clo = nullptr;
+    float jump_ms = 0;   // last async run: summed pool-lock wait / hold (device clock)
     uint32_t* a_log = nullptr;
     uint32_t a_log_cap = 0;
     unsigned long long* a_u64 = nullptr;   // flips_cum, t0, best_t
@@ -487,6 +495,15 @@ static dabs_status create_end(dabs_ctx* c)
     AB(c->a_lock, 64 * P + 96); AB(c->a_hash, P * cap); AB(c->a_u64, 12); AB(c->a_bestE, 1); AB(c->a_bestX, nwp); AB(c->a_brec, 4);
     c->a_log_cap = (uint32_t)std::max<size_t>(1u << 20, 64 * ns);
     AB(c->a_log, c->a_log_cap);
+    if (cfg.flags & DABS_FLAG_JUMP_START) {
+        c->jump = true;
+        const size_t np = (size_t)c->n_pad;
+        AB(c->Whi, np * np); AB(c->Wlo, np * np); AB(c->Dx, ns * np); AB(c->Chi, ns * np); AB(c->Clo, ns * np);
+        jump_split_kernel<<<4 * 148, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->Whi, c->Wlo);
+        if (cublasCreate(&c->cub) != CUBLAS_STATUS_SUCCESS) return bail(fail(DABS_E_CUDA, "cublasCreate failed"));
+        if (cublasSetStream(c->cub, c->stream) != CUBLAS_STATUS_SUCCESS)
+            return bail(fail(DABS_E_CUDA, "cublasSetStream failed"));
+    }
     AB(c->send, c->L.bytes);
     AB(c->recv, c->L.bytes * (size_t)cfg.world);
 #undef AB
@@ -583,6 +600,7 @@ static void dabs_destroy_impl(dabs_ctx* c)
     for (void* q : c->allocs) {
         if (c->cfg.free) c->cfg.free(c->cfg.user, q, c->stream); else cudaFree(q);
     }
+    if (c->cub) cublasDestroy(c->cub);
     for (auto& e : c->ev) if (e) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -649,6 +667,28 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     return DABS_OK;
 }
 
+// C = W . D for all slots: two exact fp16 tensor-core GEMMs (cuBLAS, library GEMM),
+// then X, Delta, E per slot (jump_kernels.cuh)
+static dabs_status jump_start(dabs_ctx* c)
+{
+    cudaStream_t st = c->stream;
+    const int np = c->n_pad;
+    jump_expand_kernel<<<c->slots, 256, 0, st>>>(c->D, c->nwp, np, c->Dx);
+    CK(cudaGetLastError());
+    const float one = 1.0f, zero = 0.0f;
+    for (int h = 0; h < 2; h++) {
+        const cublasStatus_t r = cublasGemmEx(c->cub, CUBLAS_OP_T, CUBLAS_OP_N, np, c->slots, np, &one,
+                                              h ? c->Wlo : c->Whi, CUDA_R_16F, np, c->Dx, CUDA_R_16F, np, &zero,
+                                              h ? c->Clo : c->Chi, CUDA_R_32F, np, CUBLAS_COMPUTE_32F,
+                                              CUBLAS_GEMM_DEFAULT);
+        if (r != CUBLAS_STATUS_SUCCESS) return fail(DABS_E_CUDA, "cublasGemmEx (fp16, fp32 accumulate) failed: %d", (int)r);
+    }
+    jump_finish_kernel<<<c->slots, 256, 0, st>>>(c->D, c->Chi, c->Clo, c->diag, c->n, np, c->nwp, c->X, c->delta,
+                                                 c->E);
+    CK(cudaGetLastError());
+    return DABS_OK;
+}
+
 extern "C" dabs_status dabs_generation(dabs_ctx* c)
 {
     if (!c) return fail(DABS_E_ARG, "ctx is NULL");
@@ -662,6 +702,13 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
                                                         c->gen, c->slots, c->D, c->palgo, c->pgenop,
                                                         c->dispatch);
     CK(cudaGetLastError());
+    if (c->jump) {
+        // jump-start (R-30): X = D, Delta(D), E(D) for every slot from one GEMM pair
+        CK(cudaEventRecord(c->ev[4], st));
+        dabs_status sj = jump_start(c);
+        if (sj != DABS_OK) return sj;
+        CK(cudaEventRecord(c->ev[5], st));
+    }
     CK(cudaEventRecord(c->ev[1], st));
     // a4-a7: one batch search per slot (the hot loop)
     order_kernel<<<1, 256, 0, st>>>(c->palgo, c->slots, c->order);
@@ -695,6 +742,10 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
                            cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     cudaEventElapsedTime(&c->ga_ms, c->ev[0], c->ev[1]);
+    if (c->jump) {
+        cudaEventElapsedTime(&c->jump_ms, c->ev[4], c->ev[5]);
+        if (getenv("DABS_JUMP_TIMING")) fprintf(stderr, "jump-start GEMMs + finish: %.3f ms\n", c->jump_ms);
+    }
     cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
     cudaEventElapsedTime(&c->merge_ms, c->ev[2], c->ev[3]);
     uint64_t tot = 0;
@@ -767,6 +818,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     if (c->CL != 1) return fail(DABS_E_ARG, "the asynchronous schedule needs n <= 32768 (CTA tiers)");
     if (c->cfg.restart_gens) return fail(DABS_E_ARG, "restart-on-merge is a generation-schedule option");
     if (c->trace_slot >= 0) return fail(DABS_E_ARG, "tracing is a generation-schedule option");
+    if (c->jump) return fail(DABS_E_ARG, "jump-start is a generation-schedule option");
     dabs_status st = dabs_reset(c, seed);
     if (st != DABS_OK) return st;
     const auto t0 = std::chrono::steady_clock::now();

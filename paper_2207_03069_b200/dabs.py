@@ -147,7 +147,7 @@ class Solver:
                  restart_gens: int = 0,
                  pools: int = 1, slots: int = 0, target: int | None = None, time_limit_ns: int = 0,
                  rank: int = 0, world: int = 1, device: int = -1, stream=None, exchange=None,
-                 one_wave: bool = False):
+                 one_wave: bool = False, jump: bool = False):
         L = load()
         if csr is None:
             W = np.ascontiguousarray(W, dtype=np.int16)
@@ -166,7 +166,7 @@ class Solver:
         cfg.eps_ppm, cfg.genop_mask, cfg.algo_mask = eps_ppm, genop_mask, algo_mask
         cfg.pools_per_gpu, cfg.slots_per_pool = pools, slots
         cfg.restart_gens = restart_gens
-        cfg.flags = 1 if one_wave else 0
+        cfg.flags = (1 if one_wave else 0) | (2 if jump else 0)
         cfg.target_energy = INT64_MIN if target is None else int(target)
         cfg.time_limit_ns = time_limit_ns
         cfg.rank, cfg.world, cfg.device = rank, world, device

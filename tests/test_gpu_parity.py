@@ -434,3 +434,22 @@ def test_qasp_sampled_parity(orc, lib):
         np.testing.assert_array_equal(st.delta, post["delta"])
     E, x = solver.best()
     assert solver.energy(x) == E == orc.energy(U, x)
+
+
+@pytest.mark.parametrize("n,P,S,gens", [(40, 2, 5, 5), (300, 2, 4, 3), (2100, 2, 3, 2), (5000, 1, 3, 2)])
+def test_generation_parity_jump_start(orc, lib, n, P, S, gens):
+    """SURVEY f4 jump-start (R-30): X = D, E(D), Delta(D) from the int8
+    tensor-core GEMM, then the batch; whole generations vs the oracle."""
+    rng = np.random.default_rng(n + 7)
+    U = rand_upper(rng, n, -32767, 32767) if n >= 2100 else rand_upper(rng, n, -200, 200)
+    cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=S, cap=12, jump=True)
+    sysm = orc.System(U, cfg, world=1)
+    solver = lib.Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=12, jump=True)
+    sysm.reset(31)
+    solver.reset(31)
+    for g in range(gens):
+        sysm.generation()
+        solver.generation()
+        compare_world(orc, solver, sysm.ranks[0], P, g + 1)
+    assert solver.stats().total_flips == sysm.ranks[0].total_flips
+    assert solver.best()[0] == sysm.ranks[0].best()[0]
