@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-async", action="store_true", help="skip the asynchronous-schedule line (SURVEY f1)")
+    ap.add_argument("--no-jump", action="store_true", help="skip the jump-start line (SURVEY f4)")
     return ap.parse_args()
 
 
@@ -378,6 +379,46 @@ def main():
             "what": "dabs_run_async: persistent kernel, one CTA per resident search, per-pool ticket locks, "
                     "merge/seed per batch (no generation barrier); value = flips / kernel time"}
         sa.close()
+    # ---- jump-start variant: the same generations with every
+    # batch starting at its target; X, E, Delta from two exact fp16 tensor-core
+    # GEMMs (W bytes x all targets).  Its roofline is the GEMM's: 2 GEMMs of
+    # n_pad x slots x n_pad, 2 flops per multiply-add, against the measured bf16
+    # (= fp16 dense) peak.
+    if world == 1 and not args.no_jump:
+        sj = Solver(None if csr else U, csr=csr, s_milli=meta["s_milli"], b_milli=meta["b_milli"],
+                    pools=meta.get("pools", 1), slots=args.slots or meta.get("slots", 0), jump=True,
+                    device=torch.cuda.current_device(), stream=stream.cuda_stream)
+        sj.reset(args.seed)
+        for _ in range(args.warmup):
+            sj.generation()
+        jev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        j0 = sj.stats().total_flips
+        jms = []
+        for k in range(args.steps):
+            if flush is not None:
+                with torch.cuda.stream(stream):
+                    flush.fill_(k & 0xFF)
+            jev[k][0].record(stream)
+            sj.generation()
+            jev[k][1].record(stream)
+            jms.append(sj.jump_ms())
+        torch.cuda.synchronize()
+        jt = sum(a.elapsed_time(b) for a, b in jev)
+        stj = sj.stats()
+        gemm_flops = 2 * 2 * float(sj.n_pad) * float(sj.n_pad) * sj.slots
+        tpk = float(peaks.get("bf16_tflops", 0.0)) or 2250.0
+        gms = float(np.mean(jms))
+        out["jump_start"] = {
+            "value": (stj.total_flips - j0) / (jt / 1e3), "unit": UNIT, "ms_per_step": jt / args.steps,
+            "best_energy": int(stj.best_energy), "best_energy_plain": int(st1.best_energy),
+            "generations": int(stj.generations),
+            "gemm_ms_per_step": gms, "gemm_share_of_step": gms * args.steps / jt,
+            "roofline": {"bound": "tensor", "achieved": gemm_flops / (gms / 1e3) / 1e12, "peak": tpk,
+                         "unit": "TFLOP/s", "frac": gemm_flops / (gms / 1e3) / 1e12 / tpk,
+                         "kernel": "cuBLAS fp16 GEMM x2 (+ expand/finish kernels)",
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (fp16 dense = bf16 dense)"},
+            "what": "generations with jump-start batches (X = D, E and Delta from W.D) instead of Straight"}
+        sj.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         f, dt, cores, quota = oracle_sample(U, meta, args.cpu_seconds, args.seed)
         out["cpu_baseline"] = {"value": f / dt, "unit": UNIT, "cores": cores, "kind": "oracle",

@@ -170,6 +170,10 @@ dabs_status dabs_run_async(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, u
  * (host, caller-owned; may be NULL), *len = the number of events. */
 dabs_status dabs_async_log(const dabs_ctx* ctx, uint32_t* log, int64_t cap, int64_t* len);
 
+/* Device time (CUDA events, ms) of the last generation's jump-start step
+ * (target expansion, the two GEMMs, Delta/E assembly); 0 without the flag. */
+dabs_status dabs_jump_ms(const dabs_ctx* ctx, float* ms);
+
 /* The last dabs_run_async's pool-lock profile (device clock): the sum over
  * merge events of the time spent waiting for the lock and holding it. */
 dabs_status dabs_async_lock_ns(const dabs_ctx* ctx, uint64_t* wait_ns, uint64_t* hold_ns);

@@ -892,6 +892,13 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     return dabs_best(c, best_x, best_e);
 }
 
+extern "C" dabs_status dabs_jump_ms(const dabs_ctx* c, float* ms)
+{
+    if (!c || !ms) return fail(DABS_E_ARG, "NULL argument");
+    *ms = c->jump ? c->jump_ms : 0.0f;
+    return DABS_OK;
+}
+
 extern "C" dabs_status dabs_async_lock_ns(const dabs_ctx* c, uint64_t* wait_ns, uint64_t* hold_ns)
 {
     if (!c || !wait_ns || !hold_ns) return fail(DABS_E_ARG, "NULL argument");

@@ -56,7 +56,7 @@ class dabs_stats(C.Structure):
 EXPORTS = ["dabs_config_default", "dabs_create", "dabs_create_csr", "dabs_reset", "dabs_generation", "dabs_run",
            "dabs_best", "dabs_energy", "dabs_get_stats", "dabs_debug_batch", "dabs_read_slot", "dabs_read_pool",
            "dabs_read_packet", "dabs_read_stats_pool", "dabs_trace_enable", "dabs_trace_read",
-           "dabs_run_async", "dabs_async_log", "dabs_async_lock_ns",
+           "dabs_run_async", "dabs_async_log", "dabs_async_lock_ns", "dabs_jump_ms",
            "dabs_last_error", "dabs_destroy"]
 
 _lib = None
@@ -92,6 +92,8 @@ def load(path: str = LIB_PATH):
     L.dabs_run_async.restype = st
     L.dabs_async_log.argtypes = [P, P, i64, P]
     L.dabs_async_log.restype = st
+    L.dabs_jump_ms.argtypes = [P, P]
+    L.dabs_jump_ms.restype = st
     L.dabs_async_lock_ns.argtypes = [P, P, P]
     L.dabs_async_lock_ns.restype = st
     L.dabs_best.argtypes = [P, P, P]
@@ -237,6 +239,11 @@ class Solver:
         if out.size:
             _check(load().dabs_async_log(self.h, _p(out), out.size, _p(m)))
         return out
+
+    def jump_ms(self) -> float:
+        v = np.zeros(1, np.float32)
+        _check(load().dabs_jump_ms(self.h, _p(v)))
+        return float(v[0])
 
     def async_lock_ns(self):
         w = np.zeros(1, np.uint64)
