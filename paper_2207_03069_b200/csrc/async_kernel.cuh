@@ -169,9 +169,16 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
                 for (int j = 0; j < 4; j++)
                     if (r0 + 32 * j < cap) ord_s[r0 + 32 * j] = o[j];
             }
-            bE = __ldcg(a.bestE);
-            bev = __ldcg(a.brec + 2);
-            stop0 = __ldcg(a.stop);
+            // the run best and the stop flag change under other locks: one lane
+            // reads them and broadcasts, so every branch on them is warp-uniform
+            if (lane == 0) {
+                bE = __ldcg(a.bestE);
+                bev = __ldcg(a.brec + 2);
+                stop0 = __ldcg(a.stop);
+            }
+            bE = __shfl_sync(0xffffffffu, bE, 0);
+            bev = __shfl_sync(0xffffffffu, bev, 0);
+            stop0 = __shfl_sync(0xffffffffu, stop0, 0);
             __syncwarp();
             t_B = globaltimer();
             // round B: rank of the newcomer = entries with E <= Er (older seq first, R-18);
@@ -231,7 +238,8 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         }
         e = __shfl_sync(0xffffffffu, e, 0);
         fl = __shfl_sync(0xffffffffu, fl, 0);
-        const unsigned long long t0 = a.time_limit_ns ? __ldcg(a.t0) : 0ull;
+        unsigned long long t0 = a.time_limit_ns ? __ldcg(a.t0) : 0ull;
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
         const int32_t victim = ord_s[cap - 1];
         if (ins) {
             for (int w = lane; w < nwp; w += 32) __stcg(pool.X + (size_t)victim * nwp + w, Xr[w]);
@@ -253,7 +261,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         }
         __syncwarp();
         // run best (strict improvement), flips, stop rule
-        const unsigned long long now = globaltimer();
+        const unsigned long long now = __shfl_sync(0xffffffffu, globaltimer(), 0);   // one clock read: uniform stop
         // run best = the lexicographic minimum of (E, event) over all events, i.e.
         // the first event (in log order) that reached the best energy
         // (racy pre-check: an equal energy already recorded by an earlier event needs no lock)
