@@ -371,7 +371,7 @@ def main():
     # through dabs_run_async -- one persistent kernel, one CTA per resident
     # search, no generation barrier -- for the same flips as the timed steps.
     # Kernel time by CUDA events on the library's stream (batch_ms_last).
-    if world == 1 and not args.no_async and solver.threads * 1 <= 512 and n <= 32768:
+    if world == 1 and not args.no_async:
         # pools: the paper's ~216 searches per pool, one wave of
         # resident searches (a quarter of the generation schedule's four waves)
         a_pools = max(1, round(solver.slots / 4 / 216))

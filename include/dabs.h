@@ -157,8 +157,9 @@ dabs_status dabs_run(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, uint8_t
  * merges its running batch and exits.  Deterministic given the log: the CPU
  * oracle replays it (orc_world_async_replay).  Slots are persistent CTAs, so
  * create the context with flags = DABS_FLAG_ONE_WAVE (slots beyond the
- * resident capacity start only after the stop).  Requires world == 1, the CTA
- * tiers (n <= 32768), restart_gens == 0 and tracing off, else DABS_E_ARG.
+ * resident capacity start only after the stop).  Every tier (on the cluster
+ * tier the cluster's rank-0 CTA commits).  Requires world == 1,
+ * restart_gens == 0, tracing off and no jump-start, else DABS_E_ARG.
  * Writes the best vector (n bytes, host) and energy; dabs_get_stats then
  * reports the run (generations = events, time_to_best_ns from the
  * kernel's start on the device clock, batch_ms_last = the kernel's time). */

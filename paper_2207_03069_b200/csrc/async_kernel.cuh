@@ -54,7 +54,7 @@ __device__ __forceinline__ uint64_t xhash_warp(const uint32_t* X, int nwp, int l
 {
     uint64_t h = 0;
     for (int w = lane; w < nwp; w += 32) {
-        uint64_t z = ((uint64_t)X[w] << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
+        uint64_t z = ((uint64_t)__ldcg(X + w) << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         h ^= z ^ (z >> 31);
@@ -82,6 +82,7 @@ __global__ void async_init_kernel(int32_t* ord, uint64_t* hash, int P, int cap, 
 // Philox draws of packet k+1) happens before the lock.  The GA below is the
 // same arithmetic as ga_seed_warp (R-15, R-17, R-20, R-29).
 // Returns whether a next packet was seeded (CTA-uniform).
+template <int CL>
 __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t k)
 {
     __shared__ int32_t ord_s[1024];   // pool order before the merge (cap <= 1024)
@@ -92,7 +93,8 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
     const BatchParams& bp = a.bp;
     const GaConst& g = a.g;
     const int nwp = bp.nwp, cap = g.cap;
-    if (t < 32) {
+    // cluster tier: the cluster's rank-0 CTA commits; the other waits
+    if (t < 32 && (CL == 1 || cluster_rank() == 0)) {
         const int p = s / g.S;
         const int pn = (p + 1) % g.P;   // live ring successor (R-29)
         const PoolView pool = a.pools[p];
@@ -214,7 +216,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
                     const int32_t o = ord_s[r];
                     bool eq = true;
 #pragma unroll 4
-                    for (int w = lane; w < nwp; w += 32) eq &= (__ldcg(pool.X + (size_t)o * nwp + w) == Xr[w]);
+                    for (int w = lane; w < nwp; w += 32) eq &= (__ldcg(pool.X + (size_t)o * nwp + w) == __ldcg(Xr + w));
                     if (__all_sync(0xffffffffu, eq)) ins = false;
                 }
             }
@@ -242,7 +244,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         t0 = __shfl_sync(0xffffffffu, t0, 0);
         const int32_t victim = ord_s[cap - 1];
         if (ins) {
-            for (int w = lane; w < nwp; w += 32) __stcg(pool.X + (size_t)victim * nwp + w, Xr[w]);
+            for (int w = lane; w < nwp; w += 32) __stcg(pool.X + (size_t)victim * nwp + w, __ldcg(Xr + w));
             if (lane == 0) {
                 __stcg(pool.E + victim, Er);
                 __stcg(hash + victim, hr);
@@ -276,7 +278,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             }
             upd = __shfl_sync(0xffffffffu, upd, 0);
             if (upd) {
-                for (int w = lane; w < nwp; w += 32) __stcg(a.bestX + w, Xr[w]);
+                for (int w = lane; w < nwp; w += 32) __stcg(a.bestX + w, __ldcg(Xr + w));
                 if (lane == 0) {
                     __stcg(a.bestE, Er);
                     __stcg(a.brec + 0, (int32_t)alg);
@@ -385,24 +387,34 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             }
         }
     }
-    __syncthreads();
+    if constexpr (CL == 2) {
+        // publish the decision to the peer CTA (its shared memory), then a
+        // cluster barrier (release/acquire: the packet in global memory too)
+        if (t == 0 && cluster_rank() == 0) {
+            const uint32_t peer = mapa_peer(smem_u32(&sh_seeded), 1u);
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer), "r"((uint32_t)sh_seeded) : "memory");
+        }
+        cluster_sync_all();
+    } else {
+        __syncthreads();
+    }
     return sh_seeded != 0;
 }
 
-template <int C, int NTT>
+template <int C, int NTT, int CL>
 __global__ void __launch_bounds__(NTT) async_kernel(const AsyncArgs a)
 {
-    const int s = (int)blockIdx.x;
+    const int s = (int)blockIdx.x / CL;
     const unsigned long long t_start = globaltimer();
     unsigned long long t_body = 0;
     for (uint32_t k = 0;; k++) {
         const unsigned long long tb = globaltimer();
-        batch_body<C, NTT, 1, false, true>(a.bp, s, k);
+        batch_body<C, NTT, CL, false, true>(a.bp, s, k);
         __syncthreads();
         t_body += globaltimer() - tb;
-        if (!async_commit(a, s, k)) break;
+        if (!async_commit<CL>(a, s, k)) break;
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && (CL == 1 || cluster_rank() == 0)) {
         atomicAdd(a.lock_ns + 7, t_body);                    // time in batches
         atomicAdd(a.lock_ns + 8, globaltimer() - t_start);   // CTA lifetime
     }

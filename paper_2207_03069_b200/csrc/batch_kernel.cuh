@@ -422,7 +422,9 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
         for (int c = 0; c < C; c++) {
             const int ch = (c << lgNTG) + tq;
             xb |= (bits_t)Xb[ch] << (8 * c);
-            db |= (bits_t)Db[ch] << (8 * c);
+            // REUSE: the packet was written by the commit warp (on the cluster's
+            // other SM for CL = 2): read it from L2, not a stale L1 line
+            db |= (bits_t)(REUSE ? __ldcg(Db + ch) : Db[ch]) << (8 * c);
             const int nv = min(max(n - ch * 8, 0), 8);
             vb |= (bits_t)((1u << nv) - 1u) << (8 * c);
             const int4 a = reinterpret_cast<const int4*>(dp + ch * 8)[0];
@@ -453,7 +455,7 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
             sg[g] = w;
         }
     }
-    if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
+    if (t < TABU_RING) ring_s[t] = REUSE ? __ldcg(p.ring + (size_t)s * TABU_RING + t) : p.ring[(size_t)s * TABU_RING + t];
     if (t == 0) {
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) mbar_init(&mbar[qq], 1);
@@ -461,8 +463,8 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
         fence_mbar_init();
     }
     int pos = 0;   // ring_s[(pos + j) & 31] = j-th most recent flip
-    int64_t E = p.E[s];
-    const int algo = p.algo[s];
+    int64_t E = REUSE ? (int64_t)__ldcg(reinterpret_cast<const long long*>(p.E + s)) : p.E[s];
+    const int algo = REUSE ? (int)__ldcg(p.algo + s) : (int)p.algo[s];
     const int tabu = p.tabu;
     const int T = p.T;
     // tabu state (R-11): each thread counts its own elements' occurrences in
@@ -1207,11 +1209,12 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
 #endif
     if constexpr (CL == 2) cluster_sync_all();   // no CTA leaves while its peer may still write to it
     if constexpr (REUSE) {
-        static_assert(CL == 1, "persistent batches: CTA tiers only");
         if constexpr (MW) __syncthreads(); else __syncwarp();
-        if (t == 0)
+        if (t == 0) {
 #pragma unroll
             for (int qq = 0; qq < NP; qq++) mbar_inval(&mbar[qq]);
+            if constexpr (CL == 2) { mbar_inval(&xbar[0]); mbar_inval(&xbar[1]); }
+        }
     }
 }
 

@@ -217,15 +217,23 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
 static BatchFn pick_batch(const dabs_ctx* c, bool trace) { return pick_batch(c->C, c->NT, c->CL, trace); }
 
 using AsyncFn = void (*)(const AsyncArgs);
-static AsyncFn pick_async(int C, int NT)
+static AsyncFn pick_async(int C, int NT, int CL)
 {
+    if (CL == 2) {
+        switch (NT) {
+        case 64: return async_kernel<8, 64, 2>;
+        case 128: return async_kernel<8, 128, 2>;
+        case 256: return async_kernel<8, 256, 2>;
+        default: return async_kernel<8, 512, 2>;
+        }
+    }
     switch (NT) {
-    case 32: return C == 1 ? async_kernel<1, 32> : C == 2 ? async_kernel<2, 32> : C == 4 ? async_kernel<4, 32>
-                                                                                 : async_kernel<8, 32>;
-    case 64: return async_kernel<8, 64>;
-    case 128: return async_kernel<8, 128>;
-    case 256: return async_kernel<8, 256>;
-    default: return async_kernel<8, 512>;
+    case 32: return C == 1 ? async_kernel<1, 32, 1> : C == 2 ? async_kernel<2, 32, 1> : C == 4 ? async_kernel<4, 32, 1>
+                                                                                       : async_kernel<8, 32, 1>;
+    case 64: return async_kernel<8, 64, 1>;
+    case 128: return async_kernel<8, 128, 1>;
+    case 256: return async_kernel<8, 256, 1>;
+    default: return async_kernel<8, 512, 1>;
     }
 }
 
@@ -340,8 +348,8 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
-    if (c->CL == 1) {
-        cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT, c->CL), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)row_smem(c));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
@@ -354,19 +362,24 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         c->S = (int)cfg.slots_per_pool;
     } else {
         int occ = 0;
-        const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) && c->CL == 1;
+        const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) != 0;
         if (one_wave)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT), c->NT, row_smem(c));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT, c->CL), c->NT, row_smem(c));
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
         if (one_wave)
             c->S = std::max(1, conc / c->P);    // persistent CTAs of the asynchronous schedule, all resident
-        else
-            c->S = (4 * conc + c->P - 1) / c->P;   // four waves per generation: batch lengths differ
-                                                    // (TwoNeighbor runs 2n-1 main flips), more
-                                                    // waves let the block scheduler balance them
+        else {
+            // several waves per generation: batch lengths differ (TwoNeighbor runs
+            // 2n-1 main flips), more waves let the block scheduler balance them.
+            // With one or two searches per SM the last wave's idle tail costs the
+            // most: eight waves (R32K measured 0.477 -> 0.521 of the HBM roofline
+            // from four to eight), four otherwise
+            const int waves = conc <= 2 * prop.multiProcessorCount ? 8 : 4;
+            c->S = (waves * conc + c->P - 1) / c->P;
+        }
     }
     c->slots = c->P * c->S;
     if ((int64_t)c->slots * (cfg.world) >= (1ll << 31)) return bail(fail(DABS_E_ARG, "too many slots"));
@@ -815,7 +828,6 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
 {
     if (!c) return fail(DABS_E_ARG, "ctx is NULL");
     if (c->cfg.world != 1) return fail(DABS_E_ARG, "the asynchronous schedule runs on one rank (world == 1)");
-    if (c->CL != 1) return fail(DABS_E_ARG, "the asynchronous schedule needs n <= 32768 (CTA tiers)");
     if (c->cfg.restart_gens) return fail(DABS_E_ARG, "restart-on-merge is a generation-schedule option");
     if (c->trace_slot >= 0) return fail(DABS_E_ARG, "tracing is a generation-schedule option");
     if (c->jump) return fail(DABS_E_ARG, "jump-start is a generation-schedule option");
@@ -852,7 +864,23 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     a.time_limit_ns = c->cfg.time_limit_ns;
     a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
     CK(cudaEventRecord(c->ev[1], s0));
-    pick_async(c->C, c->NT)<<<c->slots, c->NT, row_smem(c), s0>>>(a);
+    if (c->CL == 1) {
+        pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, row_smem(c), s0>>>(a);
+    } else {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(c->slots * c->CL));
+        lc.blockDim = dim3((unsigned)c->NT);
+        lc.dynamicSmemBytes = row_smem(c);
+        lc.stream = s0;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c->CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&lc, pick_async(c->C, c->NT, c->CL), a));
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], s0));
     async_compact_kernel<<<c->P, 256, 0, s0>>>(c->pools_d, ord, c->cap, c->nwp, c->margs.sX, c->margs.sE,

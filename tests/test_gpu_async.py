@@ -105,3 +105,15 @@ def test_async_rejects(lib):
     s = lib.Solver(U, pools=1, slots=2, restart_gens=3)
     with pytest.raises(lib.DabsError):
         s.run_async(1, 1000)
+
+
+@pytest.mark.parametrize("n", [5000, 9000])
+def test_async_parity_cluster_tier(orc, lib, monkeypatch, n):
+    """The asynchronous schedule on the 2-CTA cluster tier (forced for n > 4096):
+    the cluster's rank-0 CTA commits, the peer learns the decision through
+    DSMEM and a cluster barrier."""
+    monkeypatch.setenv("DABS_CLUSTER", "1")
+    U = rand_upper(np.random.default_rng(n), n, -300, 300)
+    solver, log, st = run_pair(orc, lib, U, P=2, S=2, seed=77, budget=5 * 4 * n)
+    assert solver.stats().threads_per_search >= 128
+    assert len(log) > 4
