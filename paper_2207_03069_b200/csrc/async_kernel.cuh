@@ -73,6 +73,9 @@ __global__ void async_init_kernel(int32_t* ord, uint64_t* hash, int P, int cap, 
     if (blockIdx.x == 0 && threadIdx.x == 0) *t0 = globaltimer();
 }
 
+// bytes of dynamic shared memory the commit needs (ord_s, ord_n, eqf)
+inline size_t async_commit_smem(int cap) { return (size_t)cap * 9; }
+
 // Merge + log + seed for slot s after its batch k (warp 0 of the CTA), under
 // the ticket locks of its pool and of its Xrossover partner.  The locks are held for three
 // dependent rounds of L2 loads: (A) pool order, run best, flips, stop flag,
@@ -85,9 +88,13 @@ __global__ void async_init_kernel(int32_t* ord, uint64_t* hash, int P, int cap, 
 template <int CL>
 __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t k)
 {
-    __shared__ int32_t ord_s[1024];   // pool order before the merge (cap <= 1024)
-    __shared__ int32_t ord_n[1024];   // after
-    __shared__ uint8_t eqf[1024];     // round B: 1 = same E as the newcomer, 3 = same E and hash
+    // commit scratch in the dynamic shared memory of the batch's row buffer
+    // (idle between batches; the launch sizes it to fit, async_commit_smem):
+    // static arrays here would shrink the L1 the batches use
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    int32_t* ord_s = reinterpret_cast<int32_t*>(dyn_smem);   // pool order before the merge
+    int32_t* ord_n = ord_s + a.g.cap;                         // after
+    uint8_t* eqf = reinterpret_cast<uint8_t*>(ord_n + a.g.cap);   // round B: 1 = same E, 3 = same E and hash
     __shared__ int sh_seeded;
     const int t = threadIdx.x, lane = t & 31;
     const BatchParams& bp = a.bp;
@@ -401,22 +408,28 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
     return sh_seeded != 0;
 }
 
+// register budget of the batch kernel of the same tier: warp tier C <= 4 -> 16
+// CTAs per SM (128 registers), C = 8 -> 12; CTA tiers unconstrained
 template <int C, int NTT, int CL>
-__global__ void __launch_bounds__(NTT) async_kernel(const AsyncArgs a)
+__global__ void __launch_bounds__(NTT, NTT == 32 ? (C <= 4 ? 16 : 12) : 0) async_kernel(const AsyncArgs a)
 {
     const int s = (int)blockIdx.x / CL;
     const unsigned long long t_start = globaltimer();
-    unsigned long long t_body = 0;
+    unsigned long long t_body = 0, t_commit = 0;
     for (uint32_t k = 0;; k++) {
         const unsigned long long tb = globaltimer();
         batch_body<C, NTT, CL, false, true>(a.bp, s, k);
         __syncthreads();
-        t_body += globaltimer() - tb;
-        if (!async_commit<CL>(a, s, k)) break;
+        const unsigned long long tc = globaltimer();
+        t_body += tc - tb;
+        const bool more = async_commit<CL>(a, s, k);
+        t_commit += globaltimer() - tc;
+        if (!more) break;
     }
     if (threadIdx.x == 0 && (CL == 1 || cluster_rank() == 0)) {
         atomicAdd(a.lock_ns + 7, t_body);                    // time in batches
         atomicAdd(a.lock_ns + 8, globaltimer() - t_start);   // CTA lifetime
+        atomicAdd(a.lock_ns + 9, t_commit);                  // time in commits
     }
 }
 

@@ -350,7 +350,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     }
     {
         cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT, c->CL), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)row_smem(c));
+                                             (int)std::max(row_smem(c), async_commit_smem((int)cfg.pool_capacity)));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
     c->T = flip_factor(cfg.s_milli, n);
@@ -364,7 +364,8 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         int occ = 0;
         const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) != 0;
         if (one_wave)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT, c->CL), c->NT, row_smem(c));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT, c->CL), c->NT,
+                                                          std::max(row_smem(c), async_commit_smem((int)cfg.pool_capacity)));
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
         if (occ < 1) occ = 1;
@@ -505,7 +506,7 @@ static dabs_status create_end(dabs_ctx* c)
         L.oBestX = o; o = al8(o + 4 * nwp);
         L.bytes = o;
     }
-    AB(c->a_lock, 64 * P + 96); AB(c->a_hash, P * cap); AB(c->a_u64, 12); AB(c->a_bestE, 1); AB(c->a_bestX, nwp); AB(c->a_brec, 4);
+    AB(c->a_lock, 64 * P + 96); AB(c->a_hash, P * cap); AB(c->a_u64, 13); AB(c->a_bestE, 1); AB(c->a_bestX, nwp); AB(c->a_brec, 4);
     c->a_log_cap = (uint32_t)std::max<size_t>(1u << 20, 64 * ns);
     AB(c->a_log, c->a_log_cap);
     if (cfg.flags & DABS_FLAG_JUMP_START) {
@@ -841,7 +842,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     CK(cudaGetLastError());
     int32_t* ord = c->margs.acc;   // [P][cap] scratch, free outside the generation schedule's merge
     CK(cudaMemsetAsync(c->a_lock, 0, 4 * (64 * (size_t)c->P + 96), s0));
-    CK(cudaMemsetAsync(c->a_u64, 0, 96, s0));
+    CK(cudaMemsetAsync(c->a_u64, 0, 104, s0));
     CK(cudaMemsetAsync(c->a_brec, 0xFF, 16, s0));
     const int64_t inf = E_INF;
     CK(cudaMemcpyAsync(c->a_bestE, &inf, 8, cudaMemcpyHostToDevice, s0));
@@ -864,13 +865,14 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     a.time_limit_ns = c->cfg.time_limit_ns;
     a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
     CK(cudaEventRecord(c->ev[1], s0));
+    const size_t asmem = std::max(row_smem(c), async_commit_smem(c->cap));
     if (c->CL == 1) {
-        pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, row_smem(c), s0>>>(a);
+        pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, asmem, s0>>>(a);
     } else {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)(c->slots * c->CL));
         lc.blockDim = dim3((unsigned)c->NT);
-        lc.dynamicSmemBytes = row_smem(c);
+        lc.dynamicSmemBytes = asmem;
         lc.stream = s0;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -887,12 +889,12 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
                                                 c->margs.sSeq, c->margs.sAlgo, c->margs.sGenop);
     CK(cudaGetLastError());
     uint32_t nev = 0;
-    unsigned long long u64[12];
+    unsigned long long u64[13];
     int64_t bE = E_INF;
     int32_t rec[4];
     std::vector<uint32_t> words(c->nwp);
     CK(cudaMemcpyAsync(&nev, c->a_lock + 64 * c->P, 4, cudaMemcpyDeviceToHost, s0));
-    CK(cudaMemcpyAsync(u64, c->a_u64, 96, cudaMemcpyDeviceToHost, s0));
+    CK(cudaMemcpyAsync(u64, c->a_u64, 104, cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(&bE, c->a_bestE, 8, cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(rec, c->a_brec, 16, cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(words.data(), c->a_bestX, 4 * c->nwp, cudaMemcpyDeviceToHost, s0));
@@ -915,8 +917,9 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
                 u64[5] / 1e3 / std::max(1u, nev), u64[6] / 1e3 / std::max(1u, nev), u64[7] / 1e3 / std::max(1u, nev),
                 u64[8] / 1e3 / std::max(1u, nev), u64[9] / 1e3 / std::max(1u, nev));
     if (getenv("DABS_ASYNC_PHASES"))
-        fprintf(stderr, "async CTA time: batches %.3f of lifetime; mean lifetime %.3f ms (kernel %.3f ms)\n",
-                (double)u64[10] / std::max(1ull, u64[11]), u64[11] / 1e6 / c->slots, (double)c->batch_ms);
+        fprintf(stderr, "async CTA time: batches %.3f, commits %.3f of lifetime; mean lifetime %.3f ms (kernel %.3f ms)\n",
+                (double)u64[10] / std::max(1ull, u64[11]), (double)u64[12] / std::max(1ull, u64[11]),
+                u64[11] / 1e6 / c->slots, (double)c->batch_ms);
     return dabs_best(c, best_x, best_e);
 }
 
