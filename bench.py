@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--slots", type=int, default=0, help="slots per pool (0 = library default)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample size (cpu_baseline)")
+    ap.add_argument("--ref-seconds", type=float, default=0.0,
+                    help="reference arm: oracle seconds per step (0 = sized so the run ends within minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tts", action="store_true")
@@ -153,7 +155,7 @@ def run_reference(args):
         return
     from paper_2207_03069_b200 import workloads as wl
     U, meta = wl.make(args.workload, seed=1)
-    per_step = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = args.ref_seconds or max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(U, meta, per_step / 4, args.seed)
     flips = 0

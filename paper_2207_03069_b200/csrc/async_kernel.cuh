@@ -39,7 +39,8 @@ struct AsyncArgs {
     uint32_t* bestX;                  // [nwp]
     int32_t* brec;                    // algo, genop, event, slot
     unsigned long long* best_t;       // globaltimer of the last improvement
-    unsigned long long* lock_ns;      // [2] summed lock wait and hold times (device clock)
+    unsigned long long* lock_ns;      // [10] summed lock wait/hold times, phase and CTA-time breakdown (device clock)
+    int profile;                      // 1: also accumulate the phase / CTA-time breakdown (DABS_ASYNC_PHASES)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer()
@@ -368,7 +369,13 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             sh_seeded = seeded ? 1 : 0;
             const unsigned long long t_rel = globaltimer();
             atomicAdd(a.lock_ns, t_acq - t_req);
-            atomicAdd(a.lock_ns + 2, t_B - t_acq); atomicAdd(a.lock_ns + 3, t_D - t_B); atomicAdd(a.lock_ns + 4, t_G - t_D); atomicAdd(a.lock_ns + 5, t_R - t_G); atomicAdd(a.lock_ns + 6, t_rel - t_R);
+            if (a.profile) {
+                atomicAdd(a.lock_ns + 2, t_B - t_acq);
+                atomicAdd(a.lock_ns + 3, t_D - t_B);
+                atomicAdd(a.lock_ns + 4, t_G - t_D);
+                atomicAdd(a.lock_ns + 5, t_R - t_G);
+                atomicAdd(a.lock_ns + 6, t_rel - t_R);
+            }
             atomicAdd(a.lock_ns + 1, t_rel - t_acq);
         }
         // XREAD (R-29): the partner pool's rank-r2 row fills the bits the mask
@@ -426,7 +433,7 @@ __global__ void __launch_bounds__(NTT, NTT == 32 ? (C <= 4 ? 16 : 12) : 0) async
         t_commit += globaltimer() - tc;
         if (!more) break;
     }
-    if (threadIdx.x == 0 && (CL == 1 || cluster_rank() == 0)) {
+    if (a.profile && threadIdx.x == 0 && (CL == 1 || cluster_rank() == 0)) {
         atomicAdd(a.lock_ns + 7, t_body);                    // time in batches
         atomicAdd(a.lock_ns + 8, globaltimer() - t_start);   // CTA lifetime
         atomicAdd(a.lock_ns + 9, t_commit);                  // time in commits

@@ -864,6 +864,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     a.target = c->cfg.target_energy;
     a.time_limit_ns = c->cfg.time_limit_ns;
     a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
+    a.profile = getenv("DABS_ASYNC_PHASES") ? 1 : 0;
     CK(cudaEventRecord(c->ev[1], s0));
     const size_t asmem = std::max(row_smem(c), async_commit_smem(c->cap));
     if (c->CL == 1) {
