@@ -26,6 +26,8 @@ def main():
                     help="abs: CyclicMin + mutation after crossover only (R-27); restart: DABS with "
                          "restart-on-merge after --restart-gens stalled generations (R-28)")
     ap.add_argument("--restart-gens", type=int, default=20)
+    ap.add_argument("--schedule", default="generation", choices=["generation", "async"],
+                    help="async: dabs_run_async, one wave of persistent searches (R-29)")
     args = ap.parse_args()
     U, meta = wl.make(args.workload, seed=1)
     target = meta.get("target")
@@ -36,12 +38,13 @@ def main():
         target = args.target
     mode = dict(abs=dict(genop_mask=1 << 8, algo_mask=1 << 1), restart=dict(restart_gens=args.restart_gens),
                 dabs={})[args.mode]
+    asy = args.schedule == "async"
     s = Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=args.pools, slots=args.slots,
-               target=target, time_limit_ns=int(args.limit * 1e9), **mode)
+               target=target, time_limit_ns=int(args.limit * 1e9), one_wave=asy, **mode)
     res = []
     for r in range(args.runs):
         t0 = time.perf_counter()
-        E, x = s.run(seed=1000 + r, flip_budget=1 << 62)
+        E, x = (s.run_async if asy else s.run)(seed=1000 + r, flip_budget=1 << 62)
         dt = time.perf_counter() - t0
         st = s.stats()
         ok = target is not None and E <= target
@@ -49,7 +52,8 @@ def main():
                         gens=int(st.generations), flips=int(st.total_flips), restarts=int(st.restarts)))
         print(json.dumps(res[-1]), flush=True)
     succ = [x for x in res if x["ok"]]
-    print(json.dumps({"workload": args.workload, "mode": args.mode, "target": target, "runs": args.runs,
+    print(json.dumps({"workload": args.workload, "mode": args.mode, "schedule": args.schedule, "target": target,
+                      "runs": args.runs,
                       "success_rate": len(succ) / args.runs,
                       "mean_tts_s": float(np.mean([x["tts_s"] for x in succ])) if succ else None,
                       "slots": s.slots, "pools": s.pools,
