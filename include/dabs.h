@@ -167,8 +167,11 @@ dabs_status dabs_run_async(dabs_ctx* ctx, uint64_t seed, uint64_t flip_budget, u
                            int64_t* best_e);
 
 /* The last dabs_run_async's event log, in event order: a merge is local slot
- * | (1<<31 if a next packet was seeded); an XREAD is local slot | (1<<30).  Copies min(cap, len) entries to `log`
- * (host, caller-owned; may be NULL), *len = the number of events. */
+ * | (1<<31 if a next packet was seeded); an XREAD is local slot | (1<<30).
+ * Copies min(cap, kept) entries to `log` (host, caller-owned; may be NULL);
+ * *len = the number of events.  The device keeps the first
+ * max(2^20, 64 * slots) events; a longer run is not cut short, but its log
+ * is truncated and this call then returns DABS_E_STATE (after copying). */
 dabs_status dabs_async_log(const dabs_ctx* ctx, uint32_t* log, int64_t cap, int64_t* len);
 
 /* Device time (CUDA events, ms) of the last generation's jump-start step

@@ -26,7 +26,7 @@ struct AsyncArgs {
     uint32_t* serving;                // [P*32] ticket being served
     uint32_t* evcount;                // events so far (the event index, taken under the locks)
     int32_t* best_lock;               // guards the run best
-    uint32_t* log;                    // [log_cap]
+    uint32_t* log;                    // [log_cap]; a longer run keeps going, its log is truncated
     uint32_t log_cap;
     int slots;
     unsigned long long* flips_cum;    // flips of merged batches
@@ -304,12 +304,11 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         }
         const int64_t bE2 = Er < bE ? Er : bE;
         const bool stop = stop0 != 0 || fl >= a.budget || (a.target != INT64_MIN && bE2 <= a.target) ||
-                          (a.time_limit_ns && now - t0 >= a.time_limit_ns) ||
-                          (uint64_t)e + 1 + 2 * (uint64_t)a.slots >= (uint64_t)a.log_cap;
+                          (a.time_limit_ns && now - t0 >= a.time_limit_ns);
         const bool seeded = !stop;
         if (lane == 0) {
             if (stop) __stcg(a.stop, 1);
-            __stcg(a.log + e, (uint32_t)s | (seeded ? 0x80000000u : 0u));
+            if (e < a.log_cap) __stcg(a.log + e, (uint32_t)s | (seeded ? 0x80000000u : 0u));   // full: truncated
         }
         const unsigned long long t_G = globaltimer();
         if (seeded) {
@@ -396,7 +395,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
             }
             __syncwarp();
             if (lane == 0) {
-                __stcg(a.log + e2, (uint32_t)s | 0x40000000u);
+                if (e2 < a.log_cap) __stcg(a.log + e2, (uint32_t)s | 0x40000000u);
                 unlock(pn, tk);
             }
         }

@@ -117,6 +117,7 @@ struct dabs_ctx {
     uint32_t* a_bestX = nullptr;
     int32_t* a_brec = nullptr;
     std::vector<uint32_t> a_log_h;
+    uint32_t a_events = 0;           // events of the last async run (the log keeps the first a_log_cap)
     std::chrono::steady_clock::time_point t_reset;
 };
 
@@ -903,8 +904,10 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     CK(cudaMemcpyAsync(words.data(), c->a_bestX, 4 * c->nwp, cudaMemcpyDeviceToHost, s0));
     CK(cudaStreamSynchronize(s0));
     cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
-    c->a_log_h.resize(nev);
-    if (nev) CK(cudaMemcpy(c->a_log_h.data(), c->a_log, 4 * (size_t)nev, cudaMemcpyDeviceToHost));
+    c->a_events = nev;
+    c->a_log_h.resize(std::min(nev, c->a_log_cap));
+    if (!c->a_log_h.empty())
+        CK(cudaMemcpy(c->a_log_h.data(), c->a_log, 4 * c->a_log_h.size(), cudaMemcpyDeviceToHost));
     const auto t1 = std::chrono::steady_clock::now();
     c->wall_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
     c->total_flips = c->local_flips = u64[0];
@@ -945,8 +948,11 @@ extern "C" dabs_status dabs_async_log(const dabs_ctx* c, uint32_t* log, int64_t 
 {
     if (!c || !len) return fail(DABS_E_ARG, "NULL argument");
     const int64_t m = (int64_t)c->a_log_h.size();
-    *len = m;
+    *len = (int64_t)c->a_events;
     if (log && cap > 0) memcpy(log, c->a_log_h.data(), 4 * (size_t)std::min(cap, m));
+    if ((int64_t)c->a_events > m)
+        return fail(DABS_E_STATE, "async log truncated: %lld of %u events kept (a replay needs the whole log)",
+                    (long long)m, c->a_events);
     return DABS_OK;
 }
 
