@@ -59,6 +59,10 @@ struct BatchParams {
     int64_t tr_cap;
 };
 
+#ifndef DABS_NP_MAX
+#define DABS_NP_MAX 4   // W-row pieces (one mbarrier each) per flip in the CTA tiers (A/B: -DDABS_NP_MAX=8)
+#endif
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
 {
@@ -378,7 +382,7 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
     static_assert(CL == 1 || (CL == 2 && NTT > 32), "cluster tier needs the CTA tier");
     constexpr bool MW = NTT > 32;                    // more than one warp per search
     constexpr int EPT = 8 * C;
-    constexpr int NP = MW ? (C >= 4 ? 4 : C) : 1;   // row pieces, one mbarrier each
+    constexpr int NP = MW ? (C >= DABS_NP_MAX ? DABS_NP_MAX : C) : 1;   // row pieces, one mbarrier each
     constexpr int CPP = C / NP;                      // chunks per piece
     constexpr int CW = (C + 1) / 2;                  // packed count words (two 16-bit fields)
     using bits_t = typename std::conditional<(EPT > 32), unsigned long long, uint32_t>::type;
