@@ -68,7 +68,7 @@ def test_oracle_two_ranks_gloo_equals_single_process(orc):
         p.join(120)
         assert p.exitcode == 0
     U = _instance()
-    sysm = orc.System(U, orc.Config(**CFG), world=world)
+    sysm = orc.System(U, orc.Config(**CFG, jump=jump), world=world)
     sysm.reset(99)
     for _ in range(GENS):
         sysm.generation()
@@ -84,7 +84,9 @@ def test_oracle_two_ranks_gloo_equals_single_process(orc):
 
 
 @pytest.mark.gpu
-def test_gpu_two_ranks_one_device_equals_oracle(orc):
+@pytest.mark.parametrize("jump", [False, True])
+def test_gpu_two_ranks_one_device_equals_oracle(orc, jump):
+    """(jump = True: the jump-start variant, R-30, across ranks)"""
     import torch
     from paper_2207_03069_b200 import Solver, build
     from paper_2207_03069_b200.dabs import _device_bytes
@@ -111,7 +113,7 @@ def test_gpu_two_ranks_one_device_equals_oracle(orc):
                 return 1
         return hook
 
-    solvers = [Solver(U, rank=r, world=world, exchange=make_hook(r), **CFG) for r in range(world)]
+    solvers = [Solver(U, rank=r, world=world, exchange=make_hook(r), jump=jump, **CFG) for r in range(world)]
     for s_ in solvers:
         s_.reset(99)
     errs = []
@@ -129,7 +131,7 @@ def test_gpu_two_ranks_one_device_equals_oracle(orc):
     for x in th:
         x.join(300)
     assert not errs, errs
-    sysm = orc.System(U, orc.Config(**CFG), world=world)
+    sysm = orc.System(U, orc.Config(**CFG, jump=jump), world=world)
     sysm.reset(99)
     for _ in range(GENS):
         sysm.generation()
