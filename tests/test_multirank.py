@@ -68,7 +68,7 @@ def test_oracle_two_ranks_gloo_equals_single_process(orc):
         p.join(120)
         assert p.exitcode == 0
     U = _instance()
-    sysm = orc.System(U, orc.Config(**CFG, jump=jump), world=world)
+    sysm = orc.System(U, orc.Config(**CFG), world=world)
     sysm.reset(99)
     for _ in range(GENS):
         sysm.generation()
