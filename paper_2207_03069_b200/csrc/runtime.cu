@@ -376,12 +376,11 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         else {
             // several waves per generation: batch lengths differ (TwoNeighbor runs
             // 2n-1 main flips), more waves let the block scheduler balance them.
-            // With one or two searches per SM the last wave's idle tail costs the
-            // most (R32K measured 0.477 / 0.523 / 0.536 of the HBM roofline with
-            // four / eight / sixteen waves): sixteen waves for one search per SM,
-            // eight for two, four otherwise
-            const int sms = prop.multiProcessorCount;
-            const int waves = conc <= sms ? 16 : conc <= 2 * sms ? 8 : 4;
+            // Four waves.  More waves shorten the last wave's idle tail by only
+            // 1-3 % at a fixed algorithm (tools/waves_fixed_algo.py); the larger
+            // flips/s changes seen with more slots per generation come from the
+            // adaptive algorithm mix, not from the kernels (DESIGN 5)
+            const int waves = 4;
             c->S = (waves * conc + c->P - 1) / c->P;
         }
     }

@@ -17,3 +17,4 @@ timeout 600 python bench.py --workload GS800 --no-cpu-baseline --no-e2e --no-tts
 timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_jump_r32k.csv \
   python tools/jump_bench.py R32K 3 > gpurun_out/ncu_jump.log 2>&1; echo "ncu jump rc $?"
 tail -1 gpurun_out/bench_tsp32.log | cut -c1-300; tail -1 gpurun_out/bench_gs800.log | cut -c1-300
+timeout 600 python bench.py --slots 2368 --no-cpu-baseline --no-e2e --no-tts --no-async --no-jump > gpurun_out/bench_r32k_16w.log 2>&1; tail -1 gpurun_out/bench_r32k_16w.log | cut -c1-200
