@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-tts", action="store_true")
     ap.add_argument("--no-async", action="store_true", help="skip the asynchronous-schedule line (SURVEY f1)")
     ap.add_argument("--no-jump", action="store_true", help="skip the jump-start line (SURVEY f4)")
+    ap.add_argument("--no-per-rule", action="store_true", help="skip the one-rule-per-run kernel figures")
     return ap.parse_args()
 
 
@@ -402,6 +403,29 @@ def main():
             "what": "dabs_run_async: persistent kernel, one CTA per resident search, per-pool ticket locks, "
                     "merge/seed per batch (no generation barrier); value = flips / kernel time"}
         sa.close()
+    # ---- kernel figures per selection rule: one main rule per run
+    # (algo_mask), so the adaptive mix cannot move the number;
+    # flips/s and the fraction of the 2n-byte HBM roofline, batch kernel time
+    if world == 1 and not args.no_per_rule:
+        names = ["MaxMin", "CyclicMin", "RandomMin", "PositiveMin", "TwoNeighbor"]
+        per_rule = {}
+        for a_ in range(5):
+            sr = Solver(None if csr else U, csr=csr, s_milli=meta["s_milli"], b_milli=meta["b_milli"],
+                        pools=meta.get("pools", 1), slots=args.slots or meta.get("slots", 0), algo_mask=1 << a_,
+                        device=torch.cuda.current_device(), stream=stream.cuda_stream)
+            sr.reset(args.seed)
+            sr.generation()   # from X = 0
+            fl_, ms_ = 0, 0.0
+            for _ in range(2):
+                f0 = sr.stats().local_flips
+                sr.generation()
+                st_r = sr.stats()
+                fl_ += st_r.local_flips - f0
+                ms_ += st_r.batch_ms_last
+            v_ = fl_ / (ms_ / 1e3)
+            per_rule[names[a_]] = {"flips_per_s": v_, "frac": v_ * 2 * n / 1e9 / hbm}
+            sr.close()
+        out["per_rule"] = per_rule
     # ---- jump-start variant: the same generations with every
     # batch starting at its target; X, E, Delta from two exact fp16 tensor-core
     # GEMMs (W bytes x all targets).  Its roofline is the GEMM's: 2 GEMMs of
