@@ -18,7 +18,10 @@
  * TwoNeighbor n=6 trace, the 2300>=2000 batch example
  * (P:526-531), Philox KAT vectors, closed-form rank-bias probability
  * (P:576-578), and the checked mode below (Delta recomputed from scratch by
- * direct energy differences after every flip).
+ * direct energy differences after every flip).  The asynchronous schedule
+ * (R-29, orc_world_async_*) is pinned by its one-slot equivalence with the
+ * generation schedule and the XREAD step recomputed from Philox in the test;
+ * jump-start (R-30) by equality with Straight's incremental path.
  */
 #include <stdint.h>
 #include <stdlib.h>
