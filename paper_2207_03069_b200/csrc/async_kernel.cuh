@@ -78,11 +78,11 @@ __global__ void async_init_kernel(int32_t* ord, uint64_t* hash, int P, int cap, 
 inline size_t async_commit_smem(int cap) { return (size_t)cap * 9; }
 
 // Merge + log + seed for slot s after its batch k (warp 0 of the CTA), under
-// the ticket locks of its pool and of its Xrossover partner.  The locks are held for three
-// dependent rounds of L2 loads: (A) pool order, run best, flips, stop flag,
-// the Xrossover partner's row; (B) energies and hashes of the pool entries ->
-// rank of the newcomer; (C) the chosen tags and every candidate parent row at
-// once.  Everything that does not read the pools (own result, its hash, the
+// its pool's ticket lock (an Xrossover partner in another pool is read later,
+// by the XREAD event, under that pool's lock).  The lock is held for three
+// dependent rounds of L2 loads: (A) pool order, run best, stop flag; (B)
+// energies and hashes of the pool entries -> rank of the newcomer; (C) the
+// chosen tags and every candidate parent row at once.  Everything that does not read the pools (own result, its hash, the
 // Philox draws of packet k+1) happens before the lock.  The GA below is the
 // same arithmetic as ga_seed_warp (R-15, R-17, R-20, R-29).
 // Returns whether a next packet was seeded (CTA-uniform).
