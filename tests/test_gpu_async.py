@@ -117,3 +117,49 @@ def test_async_parity_cluster_tier(orc, lib, monkeypatch, n):
     solver, log, st = run_pair(orc, lib, U, P=2, S=2, seed=77, budget=5 * 4 * n)
     assert solver.stats().threads_per_search >= 128
     assert len(log) > 4
+
+
+def test_async_full_config_tsp32(orc, lib):
+    """The bench's async launch configuration at full size (TSP32, n = 1024,
+    11 pools, one wave of ~2365 persistent searches): a short run (every slot
+    merges at least once) replayed by the oracle from the device's log."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("TSP32", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=11, one_wave=True, cap=100)
+    Eg, Xg = solver.run_async(5, 3 * solver.slots * U.shape[0])
+    log = solver.async_log()
+    check_log(log, solver.slots)
+    w = orc.World(U, orc.Config(s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=11,
+                                slots=solver.slots // 11, cap=100))
+    w.reset(5)
+    w.async_replay(log)
+    compare_world(orc, solver, w, 11, 1)
+    assert (Eg, Xg.tobytes()) == (w.best()[0], w.best()[1].tobytes())
+
+
+def test_async_r32k_sampled(orc, lib):
+    """R32K at full size (2 GiB W), one wave of 148 persistent searches: with a
+    budget of one flip every slot runs exactly its batch 0 (from X = 0, packet
+    0 drawn from the fresh pools); sampled slots recomputed by the oracle."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("R32K", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1, one_wave=True)
+    solver.run_async(11, 1)
+    log = solver.async_log()
+    assert len(log) == solver.slots and not (log & (SEEDED | XREAD)).any()
+    w = orc.World(U, orc.Config(s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1, slots=solver.slots))
+    w.reset(11)
+    w.async_begin()
+    for s in (0, solver.slots - 1):
+        opk = w.packet(s)
+        gpk = solver.read_packet(s)
+        np.testing.assert_array_equal(gpk["D"], opk["D"])
+        assert gpk["algo"] == opk["algo"]
+        st = orc.SlotState.initial(U)
+        ref = orc.batch(U, st, opk["D"], opk["algo"], T=solver.T, B=solver.B, tabu=8, seed=11, slot=s, gen=0)
+        assert ref.flips == gpk["flips"] and ref.ebest == gpk["ebest"]
+        np.testing.assert_array_equal(ref.best, gpk["best"])
+        post = solver.read_slot(s)
+        np.testing.assert_array_equal(st.x, post["x"])
+        np.testing.assert_array_equal(st.delta, post["delta"])
+        assert st.E == post["E"]
