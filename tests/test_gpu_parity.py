@@ -453,3 +453,27 @@ def test_generation_parity_jump_start(orc, lib, n, P, S, gens):
         compare_world(orc, solver, sysm.ranks[0], P, g + 1)
     assert solver.stats().total_flips == sysm.ranks[0].total_flips
     assert solver.best()[0] == sysm.ranks[0].best()[0]
+
+
+def test_r32k_sampled_parity_jump(orc, lib):
+    """Jump-start (R-30) at full size: R32K's int16 weights in [-32767, 32767]
+    exercise the exact fp16 byte-split GEMMs at their largest partial sums
+    (n * 128 = 2^22); one sampled slot of the bench launch recomputed by the
+    oracle (X = D, E and Delta from Eqs.(2)/(3), then the batch)."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("R32K", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1, jump=True)
+    solver.reset(4)
+    solver.generation()
+    s = solver.slots // 3
+    pre = solver.read_slot(s)
+    solver.generation()
+    pk = solver.read_packet(s)
+    post = solver.read_slot(s)
+    st = orc.SlotState(pre["x"].copy(), pre["delta"].copy(), pre["E"], pre["ring"].copy())
+    ref = orc.batch(U, st, pk["D"], pk["algo"], T=solver.T, B=solver.B, tabu=8, seed=4, slot=s, gen=1, jump=True)
+    assert ref.flips == pk["flips"] and ref.ebest == pk["ebest"]
+    np.testing.assert_array_equal(ref.best, pk["best"])
+    np.testing.assert_array_equal(st.x, post["x"])
+    np.testing.assert_array_equal(st.delta, post["delta"])
+    assert st.E == post["E"]
