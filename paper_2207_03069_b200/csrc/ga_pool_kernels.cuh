@@ -294,10 +294,46 @@ struct MergeArgs {
     uint8_t* sAlgo;
     uint8_t* sGenop;
     unsigned long long* inserted;
+    int32_t* mcount;          // [P] qualifying results per pool (merge_rank_kernel)
+    uint64_t* hq;             // scratch [P][S]: hashes of the qualifiers' vectors
+    uint8_t* dupf;            // scratch [P][S]: duplicate flags
     uint32_t slot_base;
     uint32_t gen;
     int S, cap, nwp;
 };
+
+// Rank the results that can enter pool p (E < E(worst entry)) by (E, slot):
+// order[rank] = slot.  One thread per result, the whole grid (blockIdx.y =
+// pool); every block streams the pool's result energies through shared
+// memory.  O(S^2) compares spread over the GPU instead of one CTA.
+__global__ void __launch_bounds__(256) merge_rank_kernel(MergeArgs a)
+{
+    const int p = blockIdx.y;
+    const int S = a.S;
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    const int64_t* eb = a.ebest + (size_t)p * S;
+    const int64_t Eworst = a.pools[p].E[a.cap - 1];
+    const int64_t e = j < S ? eb[j] : E_INF;
+    const bool q = j < S && e < Eworst;
+    __shared__ int64_t tile[1024];
+    int rank = 0;
+    for (int base = 0; base < S; base += 1024) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 1024; i += 256) tile[i] = base + i < S ? eb[base + i] : E_INF;
+        __syncthreads();
+        if (q) {
+            const int lim = min(1024, S - base);
+            for (int i = 0; i < lim; i++) {
+                const int64_t e2 = tile[i];
+                rank += (e2 < Eworst) && (e2 < e || (e2 == e && base + i < j));
+            }
+        }
+    }
+    if (q) {
+        a.order[(size_t)p * S + rank] = j;
+        atomicAdd(&a.mcount[p], 1);
+    }
+}
 
 __device__ __forceinline__ bool vec_equal_warp(const uint32_t* a, const uint32_t* b, int nwp, int lane)
 {
@@ -314,48 +350,78 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
     const int64_t* eb = a.ebest + (size_t)p * S;
     int32_t* order = a.order + (size_t)p * S;
     int32_t* acc = a.acc + (size_t)p * cap;
-    __shared__ int s_M, s_nacc;
-    const int64_t Eworst = pool.E[cap - 1];
-    if (threadIdx.x == 0) { s_M = 0; s_nacc = 0; }
+    __shared__ int s_nacc;
+    if (threadIdx.x == 0) s_nacc = 0;
     __syncthreads();
-    // rank qualifying results by (E, slot) and scatter into sorted order
-    for (int j = threadIdx.x; j < S; j += blockDim.x) {
-        const int64_t e = eb[j];
-        if (e >= Eworst) continue;
-        int rank = 0;
-        for (int j2 = 0; j2 < S; j2++) {
-            const int64_t e2 = eb[j2];
-            rank += (e2 < Eworst) && (e2 < e || (e2 == e && j2 < j));
+    // qualifying results, ranked by (E, slot) into order[] by merge_rank_kernel
+    const int M = a.mcount[p];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    uint64_t* hq = a.hq + (size_t)p * S;     // hash of qualifier o's X
+    uint8_t* dupf = a.dupf + (size_t)p * S;  // qualifier o is an (E, X) duplicate
+    // (1) hashes of the qualifiers' vectors, one warp per qualifier
+    for (int o = wid; o < M; o += nwarps) {
+        const uint32_t* xj = a.best + ((size_t)p * S + order[o]) * nwp;
+        uint64_t h = 0;
+        for (int w = lane; w < nwp; w += 32) {
+            uint64_t z = ((uint64_t)xj[w] << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            h ^= z ^ (z >> 31);
         }
-        order[rank] = j;
-        atomicAdd(&s_M, 1);
+        const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)h);
+        const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(h >> 32));
+        if (lane == 0) hq[o] = (uint64_t)hi << 32 | lo;
     }
     __syncthreads();
-    const int M = s_M;
-    // walk in order, dropping (E, X) duplicates (warp 0)
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        int nacc = 0;
-        for (int o = 0; o < M && nacc < cap; o++) {
-            const int j = order[o];
-            const int64_t e = eb[j];
-            const uint32_t* xj = a.best + ((size_t)p * S + j) * nwp;
-            bool dup = false;
-            for (int r = 0; r < cap && !dup; r++) {           // old entries
-                if (pool.E[r] == e && vec_equal_warp(pool.X + (size_t)r * nwp, xj, nwp, lane)) dup = true;
-            }
-            for (int q = nacc - 1; q >= 0 && !dup; q--) {     // accepted results (sorted by E)
-                const int jq = acc[q];
-                if (eb[jq] != e) break;
-                if (vec_equal_warp(a.best + ((size_t)p * S + jq) * nwp, xj, nwp, lane)) dup = true;
-            }
-            if (!dup) {
-                if (lane == 0) acc[nacc] = j;
-                __syncwarp();
-                nacc++;
+    // (2) duplicate flags, one warp per qualifier (R-18): a qualifier is dropped
+    // iff its (E, X) equals an old entry or an EARLIER qualifier (equality is
+    // transitive, so "an earlier accepted result" reduces to "an earlier
+    // qualifier").  Equal-E candidates by ballot; full vectors compared only
+    // for equal hashes (earlier qualifiers) or equal energies (old entries).
+    for (int o = wid; o < M; o += nwarps) {
+        const int j = order[o];
+        const int64_t e = eb[j];
+        const uint64_t h = hq[o];
+        const uint32_t* xj = a.best + ((size_t)p * S + j) * nwp;
+        bool dup = false;
+        for (int r0 = 0; r0 < cap && !dup; r0 += 32) {    // old entries
+            const int r = r0 + lane;
+            unsigned mk = __ballot_sync(0xffffffffu, r < cap && pool.E[r] == e);
+            while (mk && !dup) {
+                const int rr = r0 + __ffs(mk) - 1;
+                mk &= mk - 1;
+                if (vec_equal_warp(pool.X + (size_t)rr * nwp, xj, nwp, lane)) dup = true;
             }
         }
-        if (lane == 0) s_nacc = nacc;
+        // earlier qualifiers with the same energy are contiguous just before o
+        for (int q0 = o - 1; q0 >= 0 && !dup; q0 -= 32) {
+            const int q = q0 - lane;
+            const bool sameE = q >= 0 && eb[order[q]] == e;
+            const unsigned stopm = __ballot_sync(0xffffffffu, q >= 0 && !sameE);
+            unsigned mk = __ballot_sync(0xffffffffu, sameE && hq[q] == h);
+            if (stopm) mk &= (__ffs(stopm) == 1) ? 0u : ((1u << (__ffs(stopm) - 1)) - 1u);   // lanes before the first E change
+            while (mk && !dup) {
+                const int qq = q0 - (__ffs(mk) - 1);
+                mk &= mk - 1;
+                if (vec_equal_warp(a.best + ((size_t)p * S + order[qq]) * nwp, xj, nwp, lane)) dup = true;
+            }
+            if (stopm) break;
+        }
+        if (lane == 0) dupf[o] = dup ? 1 : 0;
+    }
+    __syncthreads();
+    // (3) the first cap non-duplicates in order (warp 0)
+    if (threadIdx.x < 32) {
+        int nacc = 0;
+        for (int o0 = 0; o0 < M && nacc < cap; o0 += 32) {
+            const int o = o0 + lane;
+            const bool keep = o < M && !dupf[o];
+            const unsigned mk = __ballot_sync(0xffffffffu, keep);
+            const int pos = nacc + __popc(mk & ((1u << lane) - 1u));
+            if (keep && pos < cap) acc[pos] = order[o];
+            nacc += __popc(mk);
+        }
+        if (lane == 0) s_nacc = nacc < cap ? nacc : cap;
     }
     __syncthreads();
     const int nacc = s_nacc;
