@@ -544,7 +544,7 @@ typedef struct {
 typedef struct {
     int n, T, B, tabu, cap;
     int16_t* U;
-    uint32_t eps_thr;             /* floor(eps * 2^32) (R-15) */
+    uint64_t eps_thr;             /* floor(eps * 2^32) (R-15); 2^32 at eps = 1, so 64-bit */
     int n_gen, gens[N_GEN];
     int n_alg, algs[N_ALG];
     int P, S, rank, world;        /* pools per rank, slots per pool */
@@ -615,7 +615,7 @@ void* orc_world_new(const int16_t* U, int n, int s_milli, int b_milli, int tabu,
     w->B = orc_flip_factor(b_milli, n);
     w->U = (int16_t*)malloc(sizeof(int16_t) * (size_t)n * n);
     memcpy(w->U, U, sizeof(int16_t) * (size_t)n * n);
-    w->eps_thr = (uint32_t)(((uint64_t)eps_ppm << 32) / 1000000u);
+    w->eps_thr = ((uint64_t)eps_ppm << 32) / 1000000u;
     for (int g = 0; g < N_GEN; g++) if (genop_mask >> g & 1) w->gens[w->n_gen++] = g;
     for (int a = 0; a < N_ALG; a++) if (algo_mask >> a & 1) w->algs[w->n_alg++] = a;
     w->pools = (pool_t*)calloc(P, sizeof(pool_t));
@@ -746,9 +746,9 @@ static void ga_seed_g(world_t* w, int s, uint32_t gen, int live_ring)
     const pool_t* succ = (p + 1 < w->P) ? &w->pools[p + 1] : (live_ring ? &w->pools[0] : &w->nbr);
     uint32_t a[4], b[4];
     rng4(w->seed, PUR_GA_CHOICE, 0, gs, gen, 0, a);
-    int genop = (a[0] < w->eps_thr) ? w->gens[pick(a[1], (uint32_t)w->n_gen)]
+    int genop = ((uint64_t)a[0] < w->eps_thr) ? w->gens[pick(a[1], (uint32_t)w->n_gen)]
                                     : pool->genop[pick(a[1], (uint32_t)cap)];
-    int algo = (a[2] < w->eps_thr) ? w->algs[pick(a[3], (uint32_t)w->n_alg)]
+    int algo = ((uint64_t)a[2] < w->eps_thr) ? w->algs[pick(a[3], (uint32_t)w->n_alg)]
                                    : pool->algo[pick(a[3], (uint32_t)cap)];
     rng4(w->seed, PUR_GA_PARENT, 0, gs, gen, 0, b);
     uint32_t r1 = rank_pick(b[0], (uint32_t)cap), r2 = rank_pick(b[1], (uint32_t)cap);

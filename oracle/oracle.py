@@ -42,8 +42,10 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB)
+        # DABS_ORACLE_LIB: a prebuilt oracle variant (tools/mutation_probe.py
+        # loads deliberately broken builds to check that the pins reject them)
+        path = os.environ.get("DABS_ORACLE_LIB") or build()
+        L = C.CDLL(path)
         P = C.c_void_p
         i32, i64, u32, u64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
         L.orc_philox.argtypes = [P, P, P]

@@ -119,7 +119,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
         const uint32_t gen1 = k + 1;
         const uint4 ga = rng4(g.seed, PUR_GA_CHOICE, 0, gs, gen1, 0);
         const uint4 gb = rng4(g.seed, PUR_GA_PARENT, 0, gs, gen1, 0);
-        const bool g_rand = ga.x < g.eps_thr, a_rand = ga.z < g.eps_thr;
+        const bool g_rand = (uint64_t)ga.x < g.eps_thr, a_rand = (uint64_t)ga.z < g.eps_thr;
         const uint32_t pg = pick_u(ga.y, (uint32_t)cap), pa = pick_u(ga.w, (uint32_t)cap);
         const uint32_t r1 = rank_pick(gb.x, (uint32_t)cap), r2 = rank_pick(gb.y, (uint32_t)cap);
         const uint32_t n = (uint32_t)g.n;

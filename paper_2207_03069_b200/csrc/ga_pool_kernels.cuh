@@ -122,7 +122,7 @@ struct PoolView {
 
 struct GaConst {
     int n, nwp, cap, P, S;
-    uint32_t eps_thr;
+    uint64_t eps_thr;   // floor(eps 2^32): 2^32 at eps = 1, so 64-bit (R-15)
     int n_gen, n_alg;
     int gens[N_GEN];
     int algs[N_ALG];
@@ -172,9 +172,9 @@ __device__ __forceinline__ void ga_seed_warp(const GaConst& g, const PoolView& p
         return ord_succ ? (uint32_t)(succ_ord_shared ? ord_succ[r] : __ldcg(ord_succ + r)) : r;
     };
     const uint4 a = rng4(g.seed, PUR_GA_CHOICE, 0, gs, gen, 0);
-    const int genop = (a.x < g.eps_thr) ? g.gens[pick_u(a.y, (uint32_t)g.n_gen)]
+    const int genop = ((uint64_t)a.x < g.eps_thr) ? g.gens[pick_u(a.y, (uint32_t)g.n_gen)]
                                         : (int)__ldcg(pool.genop + row(ord, pick_u(a.y, (uint32_t)g.cap)));
-    const int algo = (a.z < g.eps_thr) ? g.algs[pick_u(a.w, (uint32_t)g.n_alg)]
+    const int algo = ((uint64_t)a.z < g.eps_thr) ? g.algs[pick_u(a.w, (uint32_t)g.n_alg)]
                                        : (int)__ldcg(pool.algo + row(ord, pick_u(a.w, (uint32_t)g.cap)));
     const uint4 b = rng4(g.seed, PUR_GA_PARENT, 0, gs, gen, 0);
     const uint32_t r1 = rank_pick(b.x, (uint32_t)g.cap), r2 = rank_pick(b.y, (uint32_t)g.cap);

@@ -281,6 +281,14 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     if (cfg.tabu_period > 31) return fail(DABS_E_ARG, "tabu_period > 31");
     if (cfg.pool_capacity < 1 || cfg.pool_capacity > 1024) return fail(DABS_E_ARG, "pool_capacity outside [1,1024]");
     if (cfg.s_milli < 1 || cfg.b_milli < 1) return fail(DABS_E_ARG, "s and b must be positive");
+    {
+        // MaxMin's span (R-6) takes u^3 and T^3 in 64-bit words and divides
+        // through muldiv_floor, exact for T^3 <= 2^48: T = ceil(s n) <= 65536.
+        // B must fit the int flip counters of a batch.
+        const int64_t T = ((int64_t)cfg.s_milli * n + 999) / 1000, B = ((int64_t)cfg.b_milli * n + 999) / 1000;
+        if (T > 65536) return fail(DABS_E_ARG, "T = ceil(s n) = %lld > 65536", (long long)T);
+        if (B > (int64_t)1 << 30) return fail(DABS_E_ARG, "B = ceil(b n) = %lld > 2^30", (long long)B);
+    }
     if ((cfg.genop_mask & 0x1FF) == 0 || (cfg.algo_mask & 0x1F) == 0) return fail(DABS_E_ARG, "empty genop/algo mask");
     if (cfg.eps_ppm > 1000000) return fail(DABS_E_ARG, "eps_ppm > 1e6");
     if (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world) return fail(DABS_E_ARG, "bad rank/world");
@@ -390,7 +398,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     // ---- GA constants
     GaConst& g = c->ga;
     g.n = n; g.nwp = c->nwp; g.cap = c->cap; g.P = c->P; g.S = c->S;
-    g.eps_thr = (uint32_t)(((uint64_t)cfg.eps_ppm << 32) / 1000000u);
+    g.eps_thr = ((uint64_t)cfg.eps_ppm << 32) / 1000000u;
     g.n_gen = 0; g.n_alg = 0;
     for (int k = 0; k < N_GEN; k++) if (cfg.genop_mask >> k & 1) g.gens[g.n_gen++] = k;
     for (int k = 0; k < N_ALG; k++) if (cfg.algo_mask >> k & 1) g.algs[g.n_alg++] = k;
