@@ -207,6 +207,8 @@ typedef struct {
     uint64_t restarts;           /* restart-on-merge events since reset */
     int32_t n, n_pad, threads_per_search, slots, pools, T, B;
     int32_t cap;
+    uint64_t kernel_launches;    /* kernels of this library launched by the context since create
+                                    (library GEMMs not counted) */
 } dabs_stats;
 
 dabs_status dabs_get_stats(const dabs_ctx* ctx, dabs_stats* out);
@@ -241,6 +243,17 @@ dabs_status dabs_read_stats_pool(const dabs_ctx* ctx, uint32_t pool, uint64_t* d
 dabs_status dabs_trace_enable(dabs_ctx* ctx, int32_t slot, int64_t trace_cap);
 dabs_status dabs_trace_read(const dabs_ctx* ctx, int32_t* tr_bit, int64_t* tr_E, int8_t* tr_phase,
                             int64_t* count);
+
+/* ---- measurement probe (bench.py's roofline denominators) ----
+ * The achievable W-row stream bandwidth of this GPU: `ctas_per_sm` CTAs per
+ * SM copy random rows of a device buffer of rows x row_bytes bytes into
+ * shared memory with TMA bulk copies (4 pieces per row, `inflight` rows in
+ * flight per CTA, no compute), `iters` rows each; *gbps = bytes / event time.
+ * A buffer that fits L2 gives the L2 row-stream peak.  device < 0: the current
+ * device.  row_bytes must be a multiple of 64 and inflight*row_bytes <= 200 KiB,
+ * inflight in {1, 2}, else DABS_E_ARG; the buffer is allocated and freed here. */
+dabs_status dabs_probe_row_stream(int32_t device, int64_t rows, int32_t row_bytes, int32_t ctas_per_sm,
+                                  int32_t inflight, int32_t iters, double* gbps);
 
 const char* dabs_last_error(void);
 void dabs_destroy(dabs_ctx* ctx);   /* NULL-safe */

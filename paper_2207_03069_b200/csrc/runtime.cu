@@ -20,6 +20,7 @@
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
 #include "jump_kernels.cuh"
+#include "probe.cuh"
 #include <cublas_v2.h>
 
 using namespace dabs;
@@ -104,6 +105,7 @@ struct dabs_ctx {
     uint32_t* a_lock = nullptr;      // tickets [P*32], serving [P*32], evcount, stop, best lock (own lines)
     uint64_t* a_hash = nullptr;      // [P][cap]
     uint64_t a_wait_ns = 0, a_hold_ns = 0;
+    uint64_t launches = 0;           // kernels of this library launched since create (dabs_stats)
     // jump-start
     bool jump = false;
     cublasHandle_t cub = nullptr;
@@ -419,6 +421,7 @@ static dabs_status ingest_dense(dabs_ctx* c, const int16_t* W_host)
         cudaMemsetAsync(c->scratch64, 0, 32, c->stream) != cudaSuccess)
         return bail(fail(DABS_E_CUDA, "upload of W failed"));
     check_kernel<<<n, 256, 0, c->stream>>>(U, n, c->scratch64);
+    c->launches++;
     unsigned long long flags[2];
     if (cudaMemcpyAsync(flags, c->scratch64, 16, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
         cudaStreamSynchronize(c->stream) != cudaSuccess)
@@ -433,9 +436,11 @@ static dabs_status ingest_dense(dabs_ctx* c, const int16_t* W_host)
     {
         dim3 grid((c->n_pad + 31) / 32, (n + 31) / 32), blk(32, 8);
         symmetrize_kernel<<<grid, blk, 0, c->stream>>>(U, n, c->n_pad, c->W, c->diag);
+        c->launches++;
     }
     if ((st = dalloc(c, &c->rmax, n)) != DABS_OK) return bail(st);
     rowmax_kernel<<<n, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->rmax);
+    c->launches++;
     if (cudaStreamSynchronize(c->stream) != cudaSuccess)
         return bail(fail(DABS_E_CUDA, "symmetrize: %s", cudaGetErrorString(cudaGetLastError())));
     // free the staging copy
@@ -524,6 +529,7 @@ static dabs_status create_end(dabs_ctx* c)
         const size_t np = (size_t)c->n_pad;
         AB(c->Whi, np * np); AB(c->Wlo, np * np); AB(c->Dx, ns * np); AB(c->Chi, ns * np); AB(c->Clo, ns * np);
         jump_split_kernel<<<4 * 148, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->Whi, c->Wlo);
+        c->launches++;
         if (cublasCreate(&c->cub) != CUBLAS_STATUS_SUCCESS) return bail(fail(DABS_E_CUDA, "cublasCreate failed"));
         if (cublasSetStream(c->cub, c->stream) != CUBLAS_STATUS_SUCCESS)
             return bail(fail(DABS_E_CUDA, "cublasSetStream failed"));
@@ -608,7 +614,9 @@ extern "C" dabs_status dabs_create_csr(int32_t n, const int32_t* row_ptr, const 
         cudaMemsetAsync(c->W, 0, sizeof(int16_t) * (size_t)n * c->n_pad, s0) != cudaSuccess)
         return fin(fail(DABS_E_CUDA, "CSR upload failed"));
     csr_scatter_kernel<<<n, 128, 0, s0>>>(d_rp, d_col, d_val, d_diag, n, c->n_pad, c->W, c->diag);
+    c->launches++;
     rowmax_kernel<<<n, 256, 0, s0>>>(c->W, n, c->n_pad, c->rmax);
+    c->launches++;
     if (cudaStreamSynchronize(s0) != cudaSuccess)
         return fin(fail(DABS_E_CUDA, "CSR scatter: %s", cudaGetErrorString(cudaGetLastError())));
     if ((st = create_end(c)) != DABS_OK) return fin(st);
@@ -642,9 +650,11 @@ extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)
     c->gen = 0;
     init_slots_kernel<<<c->slots, 256, 0, c->stream>>>(c->slots, c->n_pad, c->nwp, c->diag, c->X, c->delta,
                                                        c->E, c->ring);
+    c->launches++;
     const uint32_t gid0 = (uint32_t)(c->cfg.rank * c->P);
     const uint32_t nbr_gid = (uint32_t)(((c->cfg.rank + 1) * c->P) % (c->cfg.world * c->P));
     init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, c->stream>>>(c->ga, c->pools_d, gid0, nbr_gid, 0u);
+    c->launches++;
     c->stall = 0;
     c->restarts = 0;
     CK(cudaMemsetAsync(c->dispatch, 0, 8 * c->P * N_ALG * N_GEN, c->stream));
@@ -672,6 +682,7 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     BatchFn fn = pick_batch(c, trace);
     if (c->CL == 1) {
         fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
+        c->launches++;
     } else {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)(count * c->CL));
@@ -686,6 +697,7 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
         lc.attrs = at;
         lc.numAttrs = 1;
         CK(cudaLaunchKernelEx(&lc, fn, p));
+        c->launches++;
     }
     CK(cudaGetLastError());
     return DABS_OK;
@@ -698,6 +710,7 @@ static dabs_status jump_start(dabs_ctx* c)
     cudaStream_t st = c->stream;
     const int np = c->n_pad;
     jump_expand_kernel<<<c->slots, 256, 0, st>>>(c->D, c->nwp, np, c->Dx);
+    c->launches++;
     CK(cudaGetLastError());
     const float one = 1.0f, zero = 0.0f;
     for (int h = 0; h < 2; h++) {
@@ -709,6 +722,7 @@ static dabs_status jump_start(dabs_ctx* c)
     }
     jump_finish_kernel<<<c->slots, 256, 0, st>>>(c->D, c->Chi, c->Clo, c->diag, c->n, np, c->nwp, c->X, c->delta,
                                                  c->E);
+    c->launches++;
     CK(cudaGetLastError());
     return DABS_OK;
 }
@@ -725,6 +739,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, st>>>(c->ga, c->pools_d, (uint32_t)(c->cfg.rank * c->slots),
                                                         c->gen, c->slots, c->D, c->palgo, c->pgenop,
                                                         c->dispatch);
+    c->launches++;
     CK(cudaGetLastError());
     if (c->jump) {
         // jump-start (R-30): X = D, Delta(D), E(D) for every slot from one GEMM pair
@@ -736,6 +751,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     CK(cudaEventRecord(c->ev[1], st));
     // a4-a7: one batch search per slot (the hot loop)
     order_kernel<<<1, 256, 0, st>>>(c->palgo, c->slots, c->order);
+    c->launches++;
     CK(cudaGetLastError());
     dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0, c->order);
     if (s1 != DABS_OK) return s1;
@@ -744,12 +760,15 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     c->margs.gen = c->gen;
     CK(cudaMemsetAsync(c->margs.mcount, 0, 4 * (size_t)c->P, st));
     merge_rank_kernel<<<dim3((c->S + 255) / 256, c->P), 256, 0, st>>>(c->margs);
+    c->launches++;
     pool_merge_kernel<<<c->P, 1024, 0, st>>>(c->margs);
+    c->launches++;
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[3], st));
     // a9: exchange
     pack_payload_kernel<<<1, 256, 0, st>>>(c->pools_d, c->P, c->cap, c->nwp, (uint32_t)(c->cfg.rank * c->P),
                                            c->flip_total, c->send, c->L);
+    c->launches++;
     CK(cudaGetLastError());
     const uint8_t* gathered = c->send;
     if (c->cfg.world > 1) {
@@ -760,6 +779,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     const int succ_rank = (c->cfg.rank + 1) % c->cfg.world;
     import_snapshot_kernel<<<8, 256, 0, st>>>(gathered + (size_t)succ_rank * c->L.bytes, c->pools_h[c->P],
                                               c->cap, c->nwp, c->L);
+    c->launches++;
     CK(cudaGetLastError());
     // summaries of all ranks to the host
     std::vector<Summary> sums(c->cfg.world);
@@ -805,9 +825,11 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     if (c->cfg.restart_gens && c->stall >= c->cfg.restart_gens) {
         init_slots_kernel<<<c->slots, 256, 0, st>>>(c->slots, c->n_pad, c->nwp, c->diag, c->X, c->delta, c->E,
                                                     c->ring);
+        c->launches++;
         const uint32_t gid0 = (uint32_t)(c->cfg.rank * c->P);
         const uint32_t nbr_gid = (uint32_t)(((c->cfg.rank + 1) * c->P) % (c->cfg.world * c->P));
         init_pools_kernel<<<dim3(c->P + 1, c->cap), 128, 0, st>>>(c->ga, c->pools_d, gid0, nbr_gid, c->gen);
+        c->launches++;
         CK(cudaGetLastError());
         c->stall = 0;
         c->restarts++;
@@ -846,19 +868,23 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     if (c->jump) return fail(DABS_E_ARG, "jump-start is a generation-schedule option");
     dabs_status st = dabs_reset(c, seed);
     if (st != DABS_OK) return st;
-    const auto t0 = std::chrono::steady_clock::now();
+    const auto t0 = std::chrono::steady_clock::now();   // the stream is idle (dabs_reset synchronised)
     cudaStream_t s0 = c->stream;
-    // packet 0 of every slot from the fresh pools
-    ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, s0>>>(c->ga, c->pools_d, 0u, 0u, c->slots, c->D, c->palgo,
-                                                        c->pgenop, c->dispatch);
-    CK(cudaGetLastError());
     int32_t* ord = c->margs.acc;   // [P][cap] scratch, free outside the generation schedule's merge
     CK(cudaMemsetAsync(c->a_lock, 0, 4 * (64 * (size_t)c->P + 96), s0));
     CK(cudaMemsetAsync(c->a_u64, 0, 104, s0));
     CK(cudaMemsetAsync(c->a_brec, 0xFF, 16, s0));
     const int64_t inf = E_INF;
     CK(cudaMemcpyAsync(c->a_bestE, &inf, 8, cudaMemcpyHostToDevice, s0));
+    // the device clock origin t0 is stamped here, before the seeding, so the
+    // time to best below spans the same work as the generation schedule's
     async_init_kernel<<<4, 256, 0, s0>>>(ord, c->a_hash, c->P, c->cap, c->a_u64 + 1);
+    c->launches++;
+    CK(cudaGetLastError());
+    // packet 0 of every slot from the fresh pools
+    ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, s0>>>(c->ga, c->pools_d, 0u, 0u, c->slots, c->D, c->palgo,
+                                                        c->pgenop, c->dispatch);
+    c->launches++;
     CK(cudaGetLastError());
     AsyncArgs a{};
     a.bp = batch_params(c, c->seed, 0u, 0);
@@ -881,6 +907,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     const size_t asmem = std::max(row_smem(c), async_commit_smem(c->cap));
     if (c->CL == 1) {
         pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, asmem, s0>>>(a);
+        c->launches++;
     } else {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)(c->slots * c->CL));
@@ -895,11 +922,13 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
         lc.attrs = at;
         lc.numAttrs = 1;
         CK(cudaLaunchKernelEx(&lc, pick_async(c->C, c->NT, c->CL), a));
+        c->launches++;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], s0));
     async_compact_kernel<<<c->P, 256, 0, s0>>>(c->pools_d, ord, c->cap, c->nwp, c->margs.sX, c->margs.sE,
                                                 c->margs.sSeq, c->margs.sAlgo, c->margs.sGenop);
+    c->launches++;
     CK(cudaGetLastError());
     uint32_t nev = 0;
     unsigned long long u64[13];
@@ -924,7 +953,12 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     c->best_E = bE;
     for (int k = 0; k < c->n; k++) c->best_X[k] = (uint8_t)((words[k >> 5] >> (k & 31)) & 1u);
     for (int j = 0; j < 4; j++) c->rec[j] = rec[j];
-    c->ttb_ns = u64[2] > u64[1] ? u64[2] - u64[1] : 0;   // device clock, from the kernel's start
+    // time to best from dabs_reset, like the generation schedule's host wall
+    // clock: (host time from reset to this call's first launch) + (device clock
+    // from the first kernel's start to the improving merge); the host-to-device
+    // launch gap between the two (a few us) is the only part not counted
+    const uint64_t pre_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t0 - c->t_reset).count();
+    c->ttb_ns = pre_ns + (u64[2] > u64[1] ? u64[2] - u64[1] : 0);
     c->a_wait_ns = u64[3];
     c->a_hold_ns = u64[4];
     if (getenv("DABS_ASYNC_PHASES"))
@@ -981,6 +1015,7 @@ extern "C" dabs_status dabs_energy(const dabs_ctx* cc, const uint8_t* x, int64_t
     CK(cudaMemcpyAsync(c->xbytes, x, c->n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->scratch64, 0, 8, c->stream));
     energy_kernel<<<c->n, 256, 0, c->stream>>>(c->W, c->diag, c->n, c->n_pad, c->xbytes, (long long*)c->scratch64);
+    const_cast<dabs_ctx*>(c)->launches++;
     CK(cudaGetLastError());
     long long v = 0;
     CK(cudaMemcpyAsync(&v, c->scratch64, 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1016,6 +1051,7 @@ extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
             }
     o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = c->NT * c->CL; o->slots = c->slots; o->pools = c->P;
     o->T = c->T; o->B = c->B; o->cap = c->cap;
+    o->kernel_launches = c->launches;
     return DABS_OK;
 }
 
@@ -1196,5 +1232,49 @@ extern "C" dabs_status dabs_trace_read(const dabs_ctx* c, int32_t* tr_bit, int64
     if (tr_E) CK(cudaMemcpy(tr_E, c->tr_E, 8 * m, cudaMemcpyDeviceToHost));
     if (tr_phase) CK(cudaMemcpy(tr_phase, c->tr_phase, m, cudaMemcpyDeviceToHost));
     if (count) *count = m;
+    return DABS_OK;
+}
+
+// ---------------------------------------------------------------- measurement probe
+extern "C" dabs_status dabs_probe_row_stream(int32_t device, int64_t rows, int32_t row_bytes, int32_t ctas_per_sm,
+                                             int32_t inflight, int32_t iters, double* gbps)
+{
+    if (!gbps || rows < 1 || row_bytes < 64 || row_bytes % 64 || ctas_per_sm < 1 || inflight < 1 || inflight > 2 ||
+        iters < 1 || (size_t)inflight * row_bytes > 200 * 1024)
+        return fail(DABS_E_ARG, "bad probe arguments");
+    if (device >= 0) CK(cudaSetDevice(device));
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    char* buf = nullptr;
+    unsigned long long* sink = nullptr;
+    const size_t bytes = (size_t)rows * row_bytes;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) return fail(DABS_E_NOMEM, "probe buffer of %zu bytes", bytes);
+    if (cudaMalloc(&sink, 8) != cudaSuccess) { cudaFree(buf); return fail(DABS_E_NOMEM, "probe sink"); }
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaMemsetAsync(buf, 1, bytes, s);
+    const size_t smem = (size_t)inflight * row_bytes;
+    cudaFuncSetAttribute(probe_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = sms * ctas_per_sm;
+    probe_rows_kernel<<<grid, 32, smem, s>>>(buf, (uint32_t)row_bytes, (uint32_t)rows, std::max(1, iters / 10),
+                                             inflight, sink);
+    cudaEventRecord(a, s);
+    probe_rows_kernel<<<grid, 32, smem, s>>>(buf, (uint32_t)row_bytes, (uint32_t)rows, iters, inflight, sink);
+    cudaEventRecord(b, s);
+    const cudaError_t e = cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(s);
+    cudaFree(sink);
+    cudaFree(buf);
+    if (e != cudaSuccess || cudaGetLastError() != cudaSuccess)
+        return fail(DABS_E_CUDA, "probe kernel: %s", cudaGetErrorString(e));
+    *gbps = (double)grid * iters * row_bytes / (ms * 1e-3) / 1e9;
     return DABS_OK;
 }

@@ -49,6 +49,7 @@ class dabs_stats(C.Structure):
         ("dispatch", (C.c_uint64 * 9) * 5), ("inserted", (C.c_uint64 * 9) * 5), ("restarts", C.c_uint64),
         ("n", C.c_int32), ("n_pad", C.c_int32), ("threads_per_search", C.c_int32), ("slots", C.c_int32),
         ("pools", C.c_int32), ("T", C.c_int32), ("B", C.c_int32), ("cap", C.c_int32),
+        ("kernel_launches", C.c_uint64),
     ]
 
 
@@ -56,7 +57,7 @@ class dabs_stats(C.Structure):
 EXPORTS = ["dabs_config_default", "dabs_create", "dabs_create_csr", "dabs_reset", "dabs_generation", "dabs_run",
            "dabs_best", "dabs_energy", "dabs_get_stats", "dabs_debug_batch", "dabs_read_slot", "dabs_read_pool",
            "dabs_read_packet", "dabs_read_stats_pool", "dabs_trace_enable", "dabs_trace_read",
-           "dabs_run_async", "dabs_async_log", "dabs_async_lock_ns", "dabs_jump_ms",
+           "dabs_run_async", "dabs_async_log", "dabs_async_lock_ns", "dabs_jump_ms", "dabs_probe_row_stream",
            "dabs_last_error", "dabs_destroy"]
 
 _lib = None
@@ -116,6 +117,8 @@ def load(path: str = LIB_PATH):
     L.dabs_trace_enable.restype = st
     L.dabs_trace_read.argtypes = [P, P, P, P, P]
     L.dabs_trace_read.restype = st
+    L.dabs_probe_row_stream.argtypes = [i32, i64, i32, i32, i32, i32, P]
+    L.dabs_probe_row_stream.restype = st
     L.dabs_last_error.argtypes = []
     L.dabs_last_error.restype = C.c_char_p
     L.dabs_destroy.argtypes = [P]
@@ -340,6 +343,14 @@ class Solver:
         _check(load().dabs_trace_read(self.h, _p(tb), _p(te), _p(tp), _p(cnt)))
         m = int(cnt[0])
         return tb[:m], te[:m], tp[:m]
+
+
+def probe_row_stream(rows: int, row_bytes: int, ctas_per_sm: int, inflight: int = 1, iters: int = 2000,
+                     device: int = -1) -> float:
+    """dabs_probe_row_stream: achievable row-stream GB/s (roofline denominator)."""
+    v = np.zeros(1, np.float64)
+    _check(load().dabs_probe_row_stream(device, rows, row_bytes, ctas_per_sm, inflight, iters, _p(v)))
+    return float(v[0])
 
 
 def torch_exchange(group=None):
