@@ -42,5 +42,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(out: str, extra=()) -> str:
+    """A/B or diagnostic build (e.g. extra = ["-DDABS_TIMING"]) into `out`;
+    load it with DABS_LIB=<out>."""
+    cmd = [NVCC, *FLAGS, *extra, *SOURCES, "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed")
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        build_variant(sys.argv[i + 1], sys.argv[i + 2:])
+    else:
+        build(force="--force" in sys.argv, verbose=True)
