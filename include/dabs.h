@@ -93,11 +93,12 @@ typedef struct {
 
 #define DABS_FLAG_ONE_WAVE 1u
 /* Jump-start batches (R-30): in every generation each
- * slot starts its batch AT its target D (X = D, E(D) and Delta(D) from exact
- * fp16 tensor-core GEMMs of W's bytes against all targets) instead of walking there
- * with Straight's flips.  A method variant (fewer flips per batch, no scans
- * along the Straight path).  Generation schedule only; needs 4 n_pad^2 bytes
- * more device memory. */
+ * slot starts its batch AT its target D (X = D, E(D) and Delta(D) from one
+ * exact int8 tensor-core contraction (tcgen05) of W's bytes against all
+ * targets) instead of walking there with Straight's flips.  A method variant
+ * (fewer flips per batch, no scans along the Straight path).  Generation
+ * schedule only; needs 2 n_pad^2 + 128 ceil(slots/128) n_pad bytes more device
+ * memory. */
 #define DABS_FLAG_JUMP_START 2u
 
 /* Fills the defaults listed above. */

@@ -303,33 +303,27 @@ struct MergeArgs {
 };
 
 // Rank the results that can enter pool p (E < E(worst entry)) by (E, slot):
-// order[rank] = slot.  One thread per result, the whole grid (blockIdx.y =
-// pool); every block streams the pool's result energies through shared
-// memory.  O(S^2) compares spread over the GPU instead of one CTA.
+// order[rank] = slot.  One WARP per result (blockIdx.y = pool), its lanes
+// striding over the pool's S result energies: O(S^2) compares spread over
+// S warps of the whole GPU (one thread per result left most SMs idle).
 __global__ void __launch_bounds__(256) merge_rank_kernel(MergeArgs a)
 {
     const int p = blockIdx.y;
     const int S = a.S;
-    const int j = blockIdx.x * 256 + threadIdx.x;
+    const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (j >= S) return;
     const int64_t* eb = a.ebest + (size_t)p * S;
     const int64_t Eworst = a.pools[p].E[a.cap - 1];
-    const int64_t e = j < S ? eb[j] : E_INF;
-    const bool q = j < S && e < Eworst;
-    __shared__ int64_t tile[1024];
+    const int64_t e = eb[j];
+    if (!(e < Eworst)) return;                       // uniform per warp
     int rank = 0;
-    for (int base = 0; base < S; base += 1024) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < 1024; i += 256) tile[i] = base + i < S ? eb[base + i] : E_INF;
-        __syncthreads();
-        if (q) {
-            const int lim = min(1024, S - base);
-            for (int i = 0; i < lim; i++) {
-                const int64_t e2 = tile[i];
-                rank += (e2 < Eworst) && (e2 < e || (e2 == e && base + i < j));
-            }
-        }
+    for (int i = lane; i < S; i += 32) {
+        const int64_t e2 = eb[i];
+        rank += (e2 < Eworst) && (e2 < e || (e2 == e && i < j));
     }
-    if (q) {
+    rank = __reduce_add_sync(0xffffffffu, (unsigned)rank);
+    if (lane == 0) {
         a.order[(size_t)p * S + rank] = j;
         atomicAdd(&a.mcount[p], 1);
     }
@@ -358,9 +352,10 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     uint64_t* hq = a.hq + (size_t)p * S;     // hash of qualifier o's X
     uint8_t* dupf = a.dupf + (size_t)p * S;  // qualifier o is an (E, X) duplicate
-    // (1) hashes of the qualifiers' vectors, one warp per qualifier
-    for (int o = wid; o < M; o += nwarps) {
-        const uint32_t* xj = a.best + ((size_t)p * S + order[o]) * nwp;
+    // (1) hashes of the qualifiers' vectors and of the old entries, one warp per vector
+    __shared__ uint64_t hold[1024];          // old entries' hashes (cap <= 1024)
+    for (int o = wid; o < M + cap; o += nwarps) {
+        const uint32_t* xj = o < M ? a.best + ((size_t)p * S + order[o]) * nwp : pool.X + (size_t)(o - M) * nwp;
         uint64_t h = 0;
         for (int w = lane; w < nwp; w += 32) {
             uint64_t z = ((uint64_t)xj[w] << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
@@ -370,7 +365,10 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
         }
         const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)h);
         const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(h >> 32));
-        if (lane == 0) hq[o] = (uint64_t)hi << 32 | lo;
+        if (lane == 0) {
+            if (o < M) hq[o] = (uint64_t)hi << 32 | lo;
+            else hold[o - M] = (uint64_t)hi << 32 | lo;
+        }
     }
     __syncthreads();
     // (2) duplicate flags, one warp per qualifier (R-18): a qualifier is dropped
@@ -386,7 +384,7 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
         bool dup = false;
         for (int r0 = 0; r0 < cap && !dup; r0 += 32) {    // old entries
             const int r = r0 + lane;
-            unsigned mk = __ballot_sync(0xffffffffu, r < cap && pool.E[r] == e);
+            unsigned mk = __ballot_sync(0xffffffffu, r < cap && pool.E[r] == e && hold[r] == h);
             while (mk && !dup) {
                 const int rr = r0 + __ffs(mk) - 1;
                 mk &= mk - 1;

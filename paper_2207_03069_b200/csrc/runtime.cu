@@ -19,9 +19,8 @@
 #include "batch_kernel.cuh"
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
-#include "jump_kernels.cuh"
+#include "jump_tc.cuh"
 #include "probe.cuh"
-#include <cublas_v2.h>
 
 using namespace dabs;
 
@@ -108,9 +107,10 @@ struct dabs_ctx {
     uint64_t launches = 0;           // kernels of this library launched since create (dabs_stats)
     // jump-start
     bool jump = false;
-    cublasHandle_t cub = nullptr;
-    __half *Whi = nullptr, *Wlo = nullptr, *Dx = nullptr;
-    float *Chi = nullptr, *Clo = nullptr;
+    int8_t* jBhi = nullptr;          // W bytes, tiled for the tcgen05 kernel (jump_tc.cuh)
+    uint8_t *jBlo = nullptr, *jA = nullptr;
+    unsigned long long* je2 = nullptr;   // 2 E(D) per slot
+    int jMT = 0;                     // 128-slot tiles
     float jump_ms = 0;   // last async run: summed pool-lock wait / hold (device clock)
     uint32_t* a_log = nullptr;
     uint32_t a_log_cap = 0;
@@ -527,12 +527,12 @@ static dabs_status create_end(dabs_ctx* c)
     if (cfg.flags & DABS_FLAG_JUMP_START) {
         c->jump = true;
         const size_t np = (size_t)c->n_pad;
-        AB(c->Whi, np * np); AB(c->Wlo, np * np); AB(c->Dx, ns * np); AB(c->Chi, ns * np); AB(c->Clo, ns * np);
-        jump_split_kernel<<<4 * 148, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->Whi, c->Wlo);
+        c->jMT = (ns + JT_M - 1) / JT_M;
+        AB(c->jBhi, np * np); AB(c->jBlo, np * np); AB(c->jA, (size_t)c->jMT * JT_M * np); AB(c->je2, ns);
+        CK(cudaMemsetAsync(c->je2, 0, 8 * (size_t)ns, c->stream));
+        jt_tile_w_kernel<<<8 * 148, 256, 0, c->stream>>>(c->W, n, c->n_pad, c->jBhi, c->jBlo);
         c->launches++;
-        if (cublasCreate(&c->cub) != CUBLAS_STATUS_SUCCESS) return bail(fail(DABS_E_CUDA, "cublasCreate failed"));
-        if (cublasSetStream(c->cub, c->stream) != CUBLAS_STATUS_SUCCESS)
-            return bail(fail(DABS_E_CUDA, "cublasSetStream failed"));
+        CK(cudaFuncSetAttribute(jt_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JT_SMEM));
     }
     AB(c->send, c->L.bytes);
     AB(c->recv, c->L.bytes * (size_t)cfg.world);
@@ -632,7 +632,6 @@ static void dabs_destroy_impl(dabs_ctx* c)
     for (void* q : c->allocs) {
         if (c->cfg.free) c->cfg.free(c->cfg.user, q, c->stream); else cudaFree(q);
     }
-    if (c->cub) cublasDestroy(c->cub);
     for (auto& e : c->ev) if (e) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -703,25 +702,19 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     return DABS_OK;
 }
 
-// C = W . D for all slots: two exact fp16 tensor-core GEMMs (cuBLAS, library GEMM),
-// then X, Delta, E per slot (jump_kernels.cuh)
+// jump-start (R-30): X = D, E(D), Delta(D) for every slot from C = D . W on the
+// tensor cores (jump_tc.cuh: tcgen05.mma kind::i8, epilogue writes Delta)
 static dabs_status jump_start(dabs_ctx* c)
 {
     cudaStream_t st = c->stream;
-    const int np = c->n_pad;
-    jump_expand_kernel<<<c->slots, 256, 0, st>>>(c->D, c->nwp, np, c->Dx);
+    const int np = c->n_pad, KT = np / JT_K, NTL = np / JT_N;
+    jt_tile_d_kernel<<<c->jMT * KT, 256, 0, st>>>(c->D, c->slots, c->nwp, np, c->jA);
+    c->launches++;
+    jt_gemm_kernel<<<c->jMT * NTL, 128, JT_SMEM, st>>>(c->jA, c->jBhi, c->jBlo, c->D, c->diag, c->n, np, c->nwp,
+                                                       c->slots, c->jMT, c->delta, c->je2);
     c->launches++;
     CK(cudaGetLastError());
-    const float one = 1.0f, zero = 0.0f;
-    for (int h = 0; h < 2; h++) {
-        const cublasStatus_t r = cublasGemmEx(c->cub, CUBLAS_OP_T, CUBLAS_OP_N, np, c->slots, np, &one,
-                                              h ? c->Wlo : c->Whi, CUDA_R_16F, np, c->Dx, CUDA_R_16F, np, &zero,
-                                              h ? c->Clo : c->Chi, CUDA_R_32F, np, CUBLAS_COMPUTE_32F,
-                                              CUBLAS_GEMM_DEFAULT);
-        if (r != CUBLAS_STATUS_SUCCESS) return fail(DABS_E_CUDA, "cublasGemmEx (fp16, fp32 accumulate) failed: %d", (int)r);
-    }
-    jump_finish_kernel<<<c->slots, 256, 0, st>>>(c->D, c->Chi, c->Clo, c->diag, c->n, np, c->nwp, c->X, c->delta,
-                                                 c->E);
+    jt_finish_kernel<<<c->slots, 256, 0, st>>>(c->D, c->slots, c->nwp, c->X, c->je2, c->E);
     c->launches++;
     CK(cudaGetLastError());
     return DABS_OK;
@@ -759,7 +752,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     // a8: pool merge
     c->margs.gen = c->gen;
     CK(cudaMemsetAsync(c->margs.mcount, 0, 4 * (size_t)c->P, st));
-    merge_rank_kernel<<<dim3((c->S + 255) / 256, c->P), 256, 0, st>>>(c->margs);
+    merge_rank_kernel<<<dim3((c->S + 7) / 8, c->P), 256, 0, st>>>(c->margs);
     c->launches++;
     pool_merge_kernel<<<c->P, 1024, 0, st>>>(c->margs);
     c->launches++;
@@ -790,7 +783,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
     cudaEventElapsedTime(&c->ga_ms, c->ev[0], c->ev[1]);
     if (c->jump) {
         cudaEventElapsedTime(&c->jump_ms, c->ev[4], c->ev[5]);
-        if (getenv("DABS_JUMP_TIMING")) fprintf(stderr, "jump-start GEMMs + finish: %.3f ms\n", c->jump_ms);
+        if (getenv("DABS_JUMP_TIMING")) fprintf(stderr, "jump-start (tcgen05 contraction + finish): %.3f ms\n", c->jump_ms);
     }
     cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
     cudaEventElapsedTime(&c->merge_ms, c->ev[2], c->ev[3]);

@@ -436,9 +436,10 @@ def test_qasp_sampled_parity(orc, lib):
     assert solver.energy(x) == E == orc.energy(U, x)
 
 
-@pytest.mark.parametrize("n,P,S,gens", [(40, 2, 5, 5), (300, 2, 4, 3), (2100, 2, 3, 2), (5000, 1, 3, 2)])
+@pytest.mark.parametrize("n,P,S,gens", [(40, 2, 5, 5), (300, 2, 4, 3), (2100, 2, 3, 2), (5000, 1, 3, 2),
+                                        (1000, 2, 150, 2)])
 def test_generation_parity_jump_start(orc, lib, n, P, S, gens):
-    """SURVEY f4 jump-start (R-30): X = D, E(D), Delta(D) from the int8
+    """SURVEY f4 jump-start (R-30): X = D, E(D), Delta(D) from the tcgen05 int8
     tensor-core GEMM, then the batch; whole generations vs the oracle."""
     rng = np.random.default_rng(n + 7)
     U = rand_upper(rng, n, -32767, 32767) if n >= 2100 else rand_upper(rng, n, -200, 200)
@@ -457,7 +458,7 @@ def test_generation_parity_jump_start(orc, lib, n, P, S, gens):
 
 def test_r32k_sampled_parity_jump(orc, lib):
     """Jump-start (R-30) at full size: R32K's int16 weights in [-32767, 32767]
-    exercise the exact fp16 byte-split GEMMs at their largest partial sums
+    exercise the exact int8 byte-split contraction at its largest partial sums
     (n * 128 = 2^22); one sampled slot of the bench launch recomputed by the
     oracle (X = D, E and Delta from Eqs.(2)/(3), then the batch)."""
     from paper_2207_03069_b200 import workloads as wl
