@@ -39,6 +39,7 @@ struct BatchParams {
     int T, B, tabu;
     uint64_t seed;
     uint32_t gen;
+    const uint32_t* gen_ptr; // graph replays: the generation index in device memory (else gen)
     uint32_t slot_base;      // global id of local slot 0
     int slot0;               // first local slot of this launch (blockIdx.x offset)
     const int32_t* order;    // optional launch order of the slots (longest batches first)
@@ -1227,7 +1228,7 @@ __global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_ke
 {
     const int sidx = (int)blockIdx.x / CL;
     const int s = p.order ? p.order[sidx] : p.slot0 + sidx;
-    batch_body<C, NTT, CL, TRACE, false>(p, s, p.gen);
+    batch_body<C, NTT, CL, TRACE, false>(p, s, p.gen_ptr ? *p.gen_ptr : p.gen);
 }
 
 }  // namespace dabs

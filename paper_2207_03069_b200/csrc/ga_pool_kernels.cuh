@@ -227,11 +227,14 @@ __device__ __forceinline__ void ga_seed_warp(const GaConst& g, const PoolView& p
 }
 
 // One warp per slot, every slot of the generation (bulk-synchronous schedule).
+// gen_ptr (CUDA-graph replays of the generation): the generation index is read
+// from device memory instead of the by-value argument.
 __global__ void ga_seed_kernel(GaConst g, const PoolView* __restrict__ pools, uint32_t slot_base,
                                uint32_t gen, int nslots, uint32_t* __restrict__ D,
                                uint8_t* __restrict__ palgo, uint8_t* __restrict__ pgenop,
-                               unsigned long long* __restrict__ dispatch)
+                               unsigned long long* __restrict__ dispatch, const uint32_t* __restrict__ gen_ptr)
 {
+    if (gen_ptr) gen = *gen_ptr;
     const int warps = blockDim.x >> 5;
     const int s = blockIdx.x * warps + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -299,6 +302,7 @@ struct MergeArgs {
     uint8_t* dupf;            // scratch [P][S]: duplicate flags
     uint32_t slot_base;
     uint32_t gen;
+    const uint32_t* gen_ptr;  // graph replays: the generation index in device memory (else gen)
     int S, cap, nwp;
 };
 
@@ -456,7 +460,8 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
                 const int j = acc[-sr - 1];
                 const int ls = p * S + j;
                 sE[r] = eb[j];
-                sSeq[r] = ((uint64_t)(a.gen + 1) << 32) | (uint64_t)(a.slot_base + (uint32_t)ls);
+                const uint32_t gen = a.gen_ptr ? *a.gen_ptr : a.gen;
+                sSeq[r] = ((uint64_t)(gen + 1) << 32) | (uint64_t)(a.slot_base + (uint32_t)ls);
                 sA[r] = a.palgo[ls];
                 sG[r] = a.pgenop[ls];
                 atomicAdd(&a.inserted[((size_t)p * N_ALG + sA[r]) * N_GEN + sG[r]], 1ull);

@@ -105,6 +105,14 @@ struct dabs_ctx {
     uint64_t* a_hash = nullptr;      // [P][cap]
     uint64_t a_wait_ns = 0, a_hold_ns = 0;
     uint64_t launches = 0;           // kernels of this library launched since create (dabs_stats)
+    // the generation as one CUDA graph (single rank, no tracing): captured once,
+    // replayed every generation; kernels read the generation index from gen_d
+    cudaGraphExec_t gexec = nullptr;
+    uint32_t* gen_d = nullptr;
+    Summary* sums_h = nullptr;       // pinned: the summaries the graph copies out
+    uint32_t* gen_h = nullptr;       // pinned: the generation index copied in before a replay
+    uint64_t graph_launches = 0;     // kernels per replay
+    bool no_graph = false;
     // jump-start
     bool jump = false;
     int8_t* jBhi = nullptr;          // W bytes, tiled for the tcgen05 kernel (jump_tc.cuh)
@@ -536,6 +544,10 @@ static dabs_status create_end(dabs_ctx* c)
     }
     AB(c->send, c->L.bytes);
     AB(c->recv, c->L.bytes * (size_t)cfg.world);
+    AB(c->gen_d, 1);
+    if (cudaMallocHost(&c->sums_h, sizeof(Summary) * (size_t)cfg.world) != cudaSuccess ||
+        cudaMallocHost(&c->gen_h, 4) != cudaSuccess)
+        return bail(fail(DABS_E_NOMEM, "pinned summaries"));
 #undef AB
     c->best_X.assign(n, 0);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DABS_E_CUDA, "create: %s", cudaGetErrorString(cudaGetLastError())));
@@ -633,6 +645,9 @@ static void dabs_destroy_impl(dabs_ctx* c)
         if (c->cfg.free) c->cfg.free(c->cfg.user, q, c->stream); else cudaFree(q);
     }
     for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->sums_h) cudaFreeHost(c->sums_h);
+    if (c->gen_h) cudaFreeHost(c->gen_h);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -674,10 +689,11 @@ extern "C" dabs_status dabs_reset(dabs_ctx* c, uint64_t seed)
 }
 
 static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0, int count, bool trace,
-                                const int32_t* order = nullptr)
+                                const int32_t* order = nullptr, const uint32_t* gen_ptr = nullptr)
 {
     BatchParams p = batch_params(c, seed, gen, slot0);
     p.order = order;
+    p.gen_ptr = gen_ptr;
     BatchFn fn = pick_batch(c, trace);
     if (c->CL == 1) {
         fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
@@ -720,44 +736,48 @@ static dabs_status jump_start(dabs_ctx* c)
     return DABS_OK;
 }
 
-extern "C" dabs_status dabs_generation(dabs_ctx* c)
+// Enqueue one generation (a3 GA seeding, a4-a7 batches, a8 merge, a9 exchange)
+// on the library's stream; graph = captured for replay (kernels read the
+// generation index from gen_d, copied in before every replay).
+static dabs_status enqueue_generation(dabs_ctx* c, bool graph)
 {
-    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
-    if (!c->ready) return fail(DABS_E_STATE, "dabs_generation before dabs_reset");
-    CK(cudaSetDevice(c->dev));
-    const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = c->stream;
+    const uint32_t* genp = graph ? c->gen_d : nullptr;
+    // inside a capture a plain event record only orders streams; the timing
+    // events must be external records to become nodes of the graph
+    const unsigned evf = graph ? cudaEventRecordExternal : cudaEventRecordDefault;
     // a3: GA seeding
-    CK(cudaEventRecord(c->ev[0], st));
+    CK(cudaEventRecordWithFlags(c->ev[0], st, evf));
     ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, st>>>(c->ga, c->pools_d, (uint32_t)(c->cfg.rank * c->slots),
                                                         c->gen, c->slots, c->D, c->palgo, c->pgenop,
-                                                        c->dispatch);
+                                                        c->dispatch, genp);
     c->launches++;
     CK(cudaGetLastError());
     if (c->jump) {
         // jump-start (R-30): X = D, Delta(D), E(D) for every slot from one GEMM pair
-        CK(cudaEventRecord(c->ev[4], st));
+        CK(cudaEventRecordWithFlags(c->ev[4], st, evf));
         dabs_status sj = jump_start(c);
         if (sj != DABS_OK) return sj;
-        CK(cudaEventRecord(c->ev[5], st));
+        CK(cudaEventRecordWithFlags(c->ev[5], st, evf));
     }
-    CK(cudaEventRecord(c->ev[1], st));
+    CK(cudaEventRecordWithFlags(c->ev[1], st, evf));
     // a4-a7: one batch search per slot (the hot loop)
     order_kernel<<<1, 256, 0, st>>>(c->palgo, c->slots, c->order);
     c->launches++;
     CK(cudaGetLastError());
-    dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0, c->order);
+    dabs_status s1 = launch_batch(c, c->seed, c->gen, 0, c->slots, c->trace_slot >= 0, c->order, genp);
     if (s1 != DABS_OK) return s1;
-    CK(cudaEventRecord(c->ev[2], st));
+    CK(cudaEventRecordWithFlags(c->ev[2], st, evf));
     // a8: pool merge
     c->margs.gen = c->gen;
+    c->margs.gen_ptr = genp;
     CK(cudaMemsetAsync(c->margs.mcount, 0, 4 * (size_t)c->P, st));
     merge_rank_kernel<<<dim3((c->S + 7) / 8, c->P), 256, 0, st>>>(c->margs);
     c->launches++;
     pool_merge_kernel<<<c->P, 1024, 0, st>>>(c->margs);
     c->launches++;
     CK(cudaGetLastError());
-    CK(cudaEventRecord(c->ev[3], st));
+    CK(cudaEventRecordWithFlags(c->ev[3], st, evf));
     // a9: exchange
     pack_payload_kernel<<<1, 256, 0, st>>>(c->pools_d, c->P, c->cap, c->nwp, (uint32_t)(c->cfg.rank * c->P),
                                            c->flip_total, c->send, c->L);
@@ -774,19 +794,60 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
                                               c->cap, c->nwp, c->L);
     c->launches++;
     CK(cudaGetLastError());
-    // summaries of all ranks to the host
-    std::vector<Summary> sums(c->cfg.world);
+    // summaries of all ranks to the host (pinned)
     for (int r = 0; r < c->cfg.world; r++)
-        CK(cudaMemcpyAsync(&sums[r], gathered + (size_t)r * c->L.bytes + c->L.oSum, sizeof(Summary),
+        CK(cudaMemcpyAsync(&c->sums_h[r], gathered + (size_t)r * c->L.bytes + c->L.oSum, sizeof(Summary),
                            cudaMemcpyDeviceToHost, st));
+    return DABS_OK;
+}
+
+extern "C" dabs_status dabs_generation(dabs_ctx* c)
+{
+    if (!c) return fail(DABS_E_ARG, "ctx is NULL");
+    if (!c->ready) return fail(DABS_E_STATE, "dabs_generation before dabs_reset");
+    CK(cudaSetDevice(c->dev));
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t st = c->stream;
+    // one CUDA graph per context (single rank, no tracing: the exchange hook and
+    // the traced kernel stay on plain launches); DABS_NO_GRAPH=1 disables it
+    const bool use_graph = c->cfg.world == 1 && c->trace_slot < 0 && !c->no_graph && !getenv("DABS_NO_GRAPH");
+    if (use_graph) {
+        if (!c->gexec) {
+            const uint64_t l0 = c->launches;
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                cudaGetLastError();            // e.g. the legacy default stream: plain launches
+                c->no_graph = true;
+                return dabs_generation(c);
+            }
+            const dabs_status se = enqueue_generation(c, true);
+            const cudaError_t ce = cudaStreamEndCapture(st, &g);
+            if (se != DABS_OK) return se;
+            if (ce != cudaSuccess) return fail(DABS_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+            const cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
+            cudaGraphDestroy(g);
+            if (ie != cudaSuccess) return fail(DABS_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+            c->graph_launches = c->launches - l0;
+            c->launches = l0;
+        }
+        *c->gen_h = c->gen;
+        CK(cudaMemcpyAsync(c->gen_d, c->gen_h, 4, cudaMemcpyHostToDevice, st));
+        CK(cudaGraphLaunch(c->gexec, st));
+        c->launches += c->graph_launches;
+    } else {
+        const dabs_status se = enqueue_generation(c, false);
+        if (se != DABS_OK) return se;
+    }
+    const uint8_t* gathered = c->cfg.world > 1 ? c->recv : c->send;
+    const Summary* sums = c->sums_h;
     CK(cudaStreamSynchronize(st));
-    cudaEventElapsedTime(&c->ga_ms, c->ev[0], c->ev[1]);
+    CK(cudaEventElapsedTime(&c->ga_ms, c->ev[0], c->ev[1]));
     if (c->jump) {
-        cudaEventElapsedTime(&c->jump_ms, c->ev[4], c->ev[5]);
+        CK(cudaEventElapsedTime(&c->jump_ms, c->ev[4], c->ev[5]));
         if (getenv("DABS_JUMP_TIMING")) fprintf(stderr, "jump-start (tcgen05 contraction + finish): %.3f ms\n", c->jump_ms);
     }
-    cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&c->merge_ms, c->ev[2], c->ev[3]);
+    CK(cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]));
+    CK(cudaEventElapsedTime(&c->merge_ms, c->ev[2], c->ev[3]));
     uint64_t tot = 0;
     int br = 0;
     for (int r = 0; r < c->cfg.world; r++) {
@@ -876,7 +937,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     CK(cudaGetLastError());
     // packet 0 of every slot from the fresh pools
     ga_seed_kernel<<<(c->slots + 7) / 8, 256, 0, s0>>>(c->ga, c->pools_d, 0u, 0u, c->slots, c->D, c->palgo,
-                                                        c->pgenop, c->dispatch);
+                                                        c->pgenop, c->dispatch, nullptr);
     c->launches++;
     CK(cudaGetLastError());
     AsyncArgs a{};
@@ -934,7 +995,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     CK(cudaMemcpyAsync(rec, c->a_brec, 16, cudaMemcpyDeviceToHost, s0));
     CK(cudaMemcpyAsync(words.data(), c->a_bestX, 4 * c->nwp, cudaMemcpyDeviceToHost, s0));
     CK(cudaStreamSynchronize(s0));
-    cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]);
+    CK(cudaEventElapsedTime(&c->batch_ms, c->ev[1], c->ev[2]));
     c->a_events = nev;
     c->a_log_h.resize(std::min(nev, c->a_log_cap));
     if (!c->a_log_h.empty())
