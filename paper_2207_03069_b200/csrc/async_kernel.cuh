@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(NTT, NTT == 32 ? (C <= 4 ? 16 : 12) : 0) async
     unsigned long long t_body = 0, t_commit = 0;
     for (uint32_t k = 0;; k++) {
         const unsigned long long tb = globaltimer();
-        batch_body<C, NTT, CL, false, true>(a.bp, s, k);
+        batch_body<C, NTT, CL, false, true>(a.bp, s, k, k == 0);
         __syncthreads();
         const unsigned long long tc = globaltimer();
         t_body += tc - tb;

@@ -378,7 +378,7 @@ __device__ __forceinline__ void mbar_inval(uint64_t* m)
 // R-29).  REUSE: the CTA runs further batches afterwards (persistent kernel),
 // so the row mbarriers are invalidated at the end.
 template <int C, int NTT, int CL, bool TRACE, bool REUSE>
-__device__ __forceinline__ void batch_body(const BatchParams& p, const int s, const uint32_t gen)
+__device__ __forceinline__ void batch_body(const BatchParams& p, const int s, const uint32_t gen, const bool first = true)
 {
     static_assert(CL == 1 || (CL == 2 && NTT > 32), "cluster tier needs the CTA tier");
     constexpr bool MW = NTT > 32;                    // more than one warp per search
@@ -461,7 +461,12 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
         }
     }
     if (t < TABU_RING) ring_s[t] = REUSE ? __ldcg(p.ring + (size_t)s * TABU_RING + t) : p.ring[(size_t)s * TABU_RING + t];
-    if (t == 0) {
+    // REUSE (persistent CTA, CL = 1): the row mbarriers live across batches
+    // (initialised by the first batch, phase parity kept in par_keep) -- no
+    // invalidate / re-init between batches
+    constexpr bool KEEP = REUSE && CL == 1;
+    __shared__ uint32_t par_keep;
+    if (t == 0 && (!KEEP || first)) {
 #pragma unroll
         for (int qq = 0; qq < NP; qq++) mbar_init(&mbar[qq], 1);
         if constexpr (CL == 2) { mbar_init(&xbar[0], 1); mbar_init(&xbar[1], 1); }
@@ -477,7 +482,7 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
 #pragma unroll
     for (int c = 0; c < C; c++) reinterpret_cast<uint2*>(tcnt)[(c << lgNT) + t] = make_uint2(0u, 0u);
     const uint32_t piece_bytes = (uint32_t)(2 * nl / NP);
-    uint32_t par_row = 0;
+    uint32_t par_row = (KEEP && !first) ? par_keep : 0u;
     int flips = 0;
     int64_t ebest = E_INF;
     bits_t bdiff = 0;              // BEST = X xor bdiff
@@ -1074,6 +1079,9 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
 #endif
         // every thread has passed the last exchange: the row buffer is free
         const bool pre_issued = MW && CL == 1 && kind == 1;
+        // warp tier: every lane has consumed the previous row (explicit for racecheck;
+        // the shuffles of the selection already order it)
+        if constexpr (!MW) __syncwarp();
         if (pre_issued) {
             mbar_wait(&mbar[0], par_row);
             DABS_TS(7);
@@ -1106,6 +1114,7 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
         }
         pos = (pos + TABU_RING - 1) & (TABU_RING - 1);
         ring_s[pos] = si;
+        if constexpr (!MW) __syncwarp();
         if (tabu > 0) {
             // tabu window (R-11): si enters, the (tabu+1)-th most recent flip leaves
             if (owns(si)) { tcnt[lidx(si)]++; tm |= ONE << lbit(si); }
@@ -1216,9 +1225,14 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
     if constexpr (REUSE) {
         if constexpr (MW) __syncthreads(); else __syncwarp();
         if (t == 0) {
+            if constexpr (KEEP) {
+                par_keep = par_row;
+            } else {
 #pragma unroll
-            for (int qq = 0; qq < NP; qq++) mbar_inval(&mbar[qq]);
-            if constexpr (CL == 2) { mbar_inval(&xbar[0]); mbar_inval(&xbar[1]); }
+                for (int qq = 0; qq < NP; qq++) mbar_inval(&mbar[qq]);
+                mbar_inval(&xbar[0]);
+                mbar_inval(&xbar[1]);
+            }
         }
     }
 }

@@ -299,6 +299,7 @@ struct MergeArgs {
     unsigned long long* inserted;
     int32_t* mcount;          // [P] qualifying results per pool (merge_rank_kernel)
     uint64_t* hq;             // scratch [P][S]: hashes of the qualifiers' vectors
+    uint64_t* hold;           // scratch [P][cap]: hashes of the old entries' vectors
     uint8_t* dupf;            // scratch [P][S]: duplicate flags
     uint32_t slot_base;
     uint32_t gen;
@@ -340,6 +341,86 @@ __device__ __forceinline__ bool vec_equal_warp(const uint32_t* a, const uint32_t
     return __all_sync(0xffffffffu, eq);
 }
 
+__device__ __forceinline__ uint64_t vec_hash_warp(const uint32_t* x, int nwp, int lane)
+{
+    uint64_t h = 0;
+    for (int w = lane; w < nwp; w += 32) {
+        uint64_t z = ((uint64_t)x[w] << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        h ^= z ^ (z >> 31);
+    }
+    const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)h);
+    const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(h >> 32));
+    return (uint64_t)hi << 32 | lo;
+}
+
+// (1) hashes of the qualifiers' vectors (hq, in rank order) and of the old
+// entries (hold), one warp per vector, the whole grid (blockIdx.y = pool)
+__global__ void __launch_bounds__(256) merge_hash_kernel(MergeArgs a)
+{
+    const int p = blockIdx.y;
+    const int S = a.S, cap = a.cap, nwp = a.nwp;
+    const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const int M = a.mcount[p];
+    if (o >= M + cap) return;
+    const uint32_t* xj = o < M ? a.best + ((size_t)p * S + a.order[(size_t)p * S + o]) * nwp
+                               : a.pools[p].X + (size_t)(o - M) * nwp;
+    const uint64_t h = vec_hash_warp(xj, nwp, lane);
+    if (lane == 0) {
+        if (o < M) a.hq[(size_t)p * S + o] = h;
+        else a.hold[(size_t)p * cap + (o - M)] = h;
+    }
+}
+
+// (2) duplicate flags, one warp per qualifier, the whole grid (R-18): a
+// qualifier is dropped iff its (E, X) equals an old entry or an EARLIER
+// qualifier (equality is transitive, so "an earlier accepted result" reduces
+// to "an earlier qualifier").  Candidates by ballot on equal (E, hash); full
+// vectors compared only for those.
+__global__ void __launch_bounds__(256) merge_dup_kernel(MergeArgs a)
+{
+    const int p = blockIdx.y;
+    const int S = a.S, cap = a.cap, nwp = a.nwp;
+    const int o = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const int M = a.mcount[p];
+    if (o >= M) return;
+    const PoolView pool = a.pools[p];
+    const int64_t* eb = a.ebest + (size_t)p * S;
+    const int32_t* order = a.order + (size_t)p * S;
+    const uint64_t* hq = a.hq + (size_t)p * S;
+    const uint64_t* hold = a.hold + (size_t)p * cap;
+    const int j = order[o];
+    const int64_t e = eb[j];
+    const uint64_t h = hq[o];
+    const uint32_t* xj = a.best + ((size_t)p * S + j) * nwp;
+    bool dup = false;
+    for (int r0 = 0; r0 < cap && !dup; r0 += 32) {    // old entries
+        const int r = r0 + lane;
+        unsigned mk = __ballot_sync(0xffffffffu, r < cap && pool.E[r] == e && hold[r] == h);
+        while (mk && !dup) {
+            const int rr = r0 + __ffs(mk) - 1;
+            mk &= mk - 1;
+            if (vec_equal_warp(pool.X + (size_t)rr * nwp, xj, nwp, lane)) dup = true;
+        }
+    }
+    // earlier qualifiers with the same energy are contiguous just before o
+    for (int q0 = o - 1; q0 >= 0 && !dup; q0 -= 32) {
+        const int q = q0 - lane;
+        const bool sameE = q >= 0 && eb[order[q]] == e;
+        const unsigned stopm = __ballot_sync(0xffffffffu, q >= 0 && !sameE);
+        unsigned mk = __ballot_sync(0xffffffffu, sameE && hq[q] == h);
+        if (stopm) mk &= (__ffs(stopm) == 1) ? 0u : ((1u << (__ffs(stopm) - 1)) - 1u);   // lanes before the first E change
+        while (mk && !dup) {
+            const int qq = q0 - (__ffs(mk) - 1);
+            mk &= mk - 1;
+            if (vec_equal_warp(a.best + ((size_t)p * S + order[qq]) * nwp, xj, nwp, lane)) dup = true;
+        }
+        if (stopm) break;
+    }
+    if (lane == 0) a.dupf[(size_t)p * S + o] = dup ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
 {
     const int p = blockIdx.x;
@@ -351,67 +432,11 @@ __global__ void __launch_bounds__(1024) pool_merge_kernel(MergeArgs a)
     __shared__ int s_nacc;
     if (threadIdx.x == 0) s_nacc = 0;
     __syncthreads();
-    // qualifying results, ranked by (E, slot) into order[] by merge_rank_kernel
+    // qualifying results, ranked by (E, slot) into order[] by merge_rank_kernel,
+    // duplicate flags from merge_hash_kernel + merge_dup_kernel
     const int M = a.mcount[p];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    uint64_t* hq = a.hq + (size_t)p * S;     // hash of qualifier o's X
-    uint8_t* dupf = a.dupf + (size_t)p * S;  // qualifier o is an (E, X) duplicate
-    // (1) hashes of the qualifiers' vectors and of the old entries, one warp per vector
-    __shared__ uint64_t hold[1024];          // old entries' hashes (cap <= 1024)
-    for (int o = wid; o < M + cap; o += nwarps) {
-        const uint32_t* xj = o < M ? a.best + ((size_t)p * S + order[o]) * nwp : pool.X + (size_t)(o - M) * nwp;
-        uint64_t h = 0;
-        for (int w = lane; w < nwp; w += 32) {
-            uint64_t z = ((uint64_t)xj[w] << 32 | (uint32_t)w) + 0x9E3779B97F4A7C15ull;
-            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-            h ^= z ^ (z >> 31);
-        }
-        const uint32_t lo = __reduce_xor_sync(0xffffffffu, (uint32_t)h);
-        const uint32_t hi = __reduce_xor_sync(0xffffffffu, (uint32_t)(h >> 32));
-        if (lane == 0) {
-            if (o < M) hq[o] = (uint64_t)hi << 32 | lo;
-            else hold[o - M] = (uint64_t)hi << 32 | lo;
-        }
-    }
-    __syncthreads();
-    // (2) duplicate flags, one warp per qualifier (R-18): a qualifier is dropped
-    // iff its (E, X) equals an old entry or an EARLIER qualifier (equality is
-    // transitive, so "an earlier accepted result" reduces to "an earlier
-    // qualifier").  Equal-E candidates by ballot; full vectors compared only
-    // for equal hashes (earlier qualifiers) or equal energies (old entries).
-    for (int o = wid; o < M; o += nwarps) {
-        const int j = order[o];
-        const int64_t e = eb[j];
-        const uint64_t h = hq[o];
-        const uint32_t* xj = a.best + ((size_t)p * S + j) * nwp;
-        bool dup = false;
-        for (int r0 = 0; r0 < cap && !dup; r0 += 32) {    // old entries
-            const int r = r0 + lane;
-            unsigned mk = __ballot_sync(0xffffffffu, r < cap && pool.E[r] == e && hold[r] == h);
-            while (mk && !dup) {
-                const int rr = r0 + __ffs(mk) - 1;
-                mk &= mk - 1;
-                if (vec_equal_warp(pool.X + (size_t)rr * nwp, xj, nwp, lane)) dup = true;
-            }
-        }
-        // earlier qualifiers with the same energy are contiguous just before o
-        for (int q0 = o - 1; q0 >= 0 && !dup; q0 -= 32) {
-            const int q = q0 - lane;
-            const bool sameE = q >= 0 && eb[order[q]] == e;
-            const unsigned stopm = __ballot_sync(0xffffffffu, q >= 0 && !sameE);
-            unsigned mk = __ballot_sync(0xffffffffu, sameE && hq[q] == h);
-            if (stopm) mk &= (__ffs(stopm) == 1) ? 0u : ((1u << (__ffs(stopm) - 1)) - 1u);   // lanes before the first E change
-            while (mk && !dup) {
-                const int qq = q0 - (__ffs(mk) - 1);
-                mk &= mk - 1;
-                if (vec_equal_warp(a.best + ((size_t)p * S + order[qq]) * nwp, xj, nwp, lane)) dup = true;
-            }
-            if (stopm) break;
-        }
-        if (lane == 0) dupf[o] = dup ? 1 : 0;
-    }
-    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint8_t* dupf = a.dupf + (size_t)p * S;
     // (3) the first cap non-duplicates in order (warp 0)
     if (threadIdx.x < 32) {
         int nacc = 0;

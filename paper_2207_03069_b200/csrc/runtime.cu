@@ -511,7 +511,7 @@ static dabs_status create_end(dabs_ctx* c)
     MergeArgs& m = c->margs;
     m.pools = c->pools_d; m.best = c->best; m.ebest = c->ebest; m.palgo = c->palgo; m.pgenop = c->pgenop;
     AB(m.order, ns); AB(m.acc, P * cap); AB(m.sX, P * cap * nwp); AB(m.sE, P * cap); AB(m.sSeq, P * cap);
-    AB(m.sAlgo, P * cap); AB(m.sGenop, P * cap); AB(m.mcount, P); AB(m.hq, P * ns); AB(m.dupf, P * ns);
+    AB(m.sAlgo, P * cap); AB(m.sGenop, P * cap); AB(m.mcount, P); AB(m.hq, P * ns); AB(m.hold, P * cap); AB(m.dupf, P * ns);
     m.inserted = c->inserted;
     m.slot_base = (uint32_t)(cfg.rank * c->slots);
     m.S = c->S; m.cap = c->cap; m.nwp = c->nwp;
@@ -773,6 +773,10 @@ static dabs_status enqueue_generation(dabs_ctx* c, bool graph)
     c->margs.gen_ptr = genp;
     CK(cudaMemsetAsync(c->margs.mcount, 0, 4 * (size_t)c->P, st));
     merge_rank_kernel<<<dim3((c->S + 7) / 8, c->P), 256, 0, st>>>(c->margs);
+    c->launches++;
+    merge_hash_kernel<<<dim3((c->S + c->cap + 7) / 8, c->P), 256, 0, st>>>(c->margs);
+    c->launches++;
+    merge_dup_kernel<<<dim3((c->S + 7) / 8, c->P), 256, 0, st>>>(c->margs);
     c->launches++;
     pool_merge_kernel<<<c->P, 1024, 0, st>>>(c->margs);
     c->launches++;

@@ -149,3 +149,60 @@ def test_gpu_two_ranks_one_device_equals_oracle(orc, jump):
             np.testing.assert_array_equal(g["E"], o["E"])
             np.testing.assert_array_equal(g["X"], o["X"])
             np.testing.assert_array_equal(g["seq"], o["seq"])
+
+
+def _torch_exchange_worker(rank, world, port, backend, out):
+    """One process per rank, both on cuda:0, exchanging through the library's
+    torch_exchange hook (all_gather_into_tensor on the library's stream) --
+    the code path the multi-GPU bench uses with NCCL."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    from paper_2207_03069_b200 import Solver, torch_exchange
+    stream = torch.cuda.Stream()
+    s = Solver(_instance(), rank=rank, world=world, exchange=torch_exchange(), stream=stream.cuda_stream, **CFG)
+    s.reset(99)
+    for _ in range(GENS):
+        s.generation()
+    E, X = s.best()
+    st = s.stats()
+    pools = [s.read_pool(p)["E"].tolist() for p in range(CFG["pools"] + 1)]
+    out[rank] = (E, X.tolist(), (st.best_algo, st.best_genop, st.best_generation, st.best_slot), pools,
+                 int(st.total_flips))
+    s.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_torch_exchange_two_processes_equals_oracle(orc):
+    """torch_exchange (the NCCL hook of the multi-GPU bench) driven by two real
+    processes: NCCL needs one GPU per rank, so on the one-GPU box the same hook
+    runs over gloo with CUDA tensors.  Pools, bests, first-best records and
+    flip counts must equal the oracle's two-rank simulation."""
+    from paper_2207_03069_b200 import build
+    build.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    ps = [ctx.Process(target=_torch_exchange_worker, args=(r, world, port, "gloo", out)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(600)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
+    sysm = orc.System(_instance(), orc.Config(**CFG), world=world)
+    sysm.reset(99)
+    for _ in range(GENS):
+        sysm.generation()
+    for r in range(world):
+        E, X, rec = sysm.ranks[r].best()
+        gE, gX, grec, gpools, gflips = out[r]
+        assert gE == E and gX == X.tolist()
+        assert grec == (rec["algo"], rec["genop"], rec["gen"], rec["slot"])
+        assert gflips == sysm.ranks[r].total_flips
+        for p in range(CFG["pools"] + 1):
+            assert gpools[p] == sysm.ranks[r].pool(p)["E"].tolist()

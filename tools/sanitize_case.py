@@ -3,7 +3,9 @@
     compute-sanitizer --tool racecheck python tools/sanitize_case.py async
 cases: async   -- dabs_run_async, n = 96, 2 pools, one wave (ticket locks, pool merge)
        cluster -- generations on the forced 2-CTA cluster tier, n = 5000 (DSMEM swaps, mbarriers)
-       cta     -- generations on the 512-thread CTA tier, n = 20000 (TMA rows, CTA exchange)
+       cta     -- the 512-thread CTA tier (R32K's), n = 16385 (TMA rows, CTA exchange): a batch
+                  to a local minimum, then a short checked batch (sanitize only the 2nd batch_kernel
+                  launch: --kernel-name kns=batch_kernel --launch-skip 1 --launch-count 1)
        warp    -- generations on the warp tier, n = 1000
 Each case also checks its result against the CPU oracle (so a run that the
 tool perturbs into a wrong answer fails loudly)."""
@@ -19,7 +21,7 @@ def main(case):
     from paper_2207_03069_b200 import Solver, workloads as wl
     if case == "cluster":
         os.environ["DABS_CLUSTER"] = "1"
-    n = {"async": 96, "cluster": 5000, "cta": 20000, "warp": 1000}[case]
+    n = {"async": 96, "cluster": 5000, "cta": 16385, "warp": 1000}[case]
     U = wl.random_dense(n, seed=3, lo=-200, hi=200)
     if case == "async":
         s = Solver(U, s_milli=100, b_milli=1000, pools=2, one_wave=True, cap=16)
@@ -30,10 +32,25 @@ def main(case):
         w.async_replay(log)
         Eo, _, _ = w.best()
         assert E == Eo, (E, Eo)
+    elif case == "cta":
+        s = Solver(U, s_milli=5, b_milli=20, pools=1, slots=1)
+        rng = np.random.default_rng(1)
+        st = orc.SlotState.initial(U)
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        g = s.debug_batch(0, st.x, st.delta, st.E, st.ring, D, 1, seed=1, gen=0)
+        st = orc.SlotState(g["x"], g["delta"], g["E"], g["ring"])
+        D = st.x.copy()
+        D[rng.choice(n, 20, replace=False)] ^= 1
+        for algo in (1,):
+            ref_st = st.copy()
+            ref = orc.batch(U, ref_st, D, algo, T=s.T, B=s.B, tabu=8, seed=3, slot=0, gen=1)
+            got = s.debug_batch(0, st.x, st.delta, st.E, st.ring, D, algo, seed=3, gen=1)
+            assert got["flips"] == ref.flips and got["ebest"] == ref.ebest
+            assert np.array_equal(got["delta"], ref_st.delta)
     else:
         P, S = 2, 3
-        s = Solver(U, s_milli=100, b_milli=1000 if case != "cta" else 50, pools=P, slots=S, cap=16)
-        cfg = orc.Config(s_milli=100, b_milli=1000 if case != "cta" else 50, pools=P, slots=S, cap=16)
+        s = Solver(U, s_milli=100, b_milli=1000, pools=P, slots=S, cap=16)
+        cfg = orc.Config(s_milli=100, b_milli=1000, pools=P, slots=S, cap=16)
         sysm = orc.System(U, cfg, world=1)
         s.reset(9)
         sysm.reset(9)
