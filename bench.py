@@ -425,17 +425,19 @@ def main():
             traffic_src = (f"ncu --set full capture {os.path.relpath(prof_f, ROOT)}: {per_flip:.0f} "
                            f"{'L2' if l2_resident and 'l2_bytes_per_flip' in prof else 'DRAM'} bytes per flip "
                            "x flips per launch")
+    # the generation schedule's search kernel for this tier (runtime.cu pick_batch)
+    kname = "tm_batch_kernel" if (n > 16384 and solver.threads == 256) else "batch_kernel"
     if l2_resident:
         l2 = l2_row_stream_peak(n, 2 * solver.n_pad)
         roofline = {"bound": "l2", "achieved": achieved, "peak": l2["gbps"], "unit": "GB/s",
                     "frac": achieved / l2["gbps"], "traffic": traffic, "traffic_source": traffic_src,
-                    "kernel": "batch_kernel",
+                    "kernel": kname,
                     "peak_source": (f"measured live: dabs_probe_row_stream, {l2['rows']} rows x {l2['row_bytes']} B "
                                     f"(this workload's W), TMA bulk row copies, {l2['ctas_per_sm']} CTAs/SM"),
                     "hbm_frac_context": achieved / hbm}
     else:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "traffic": traffic, "traffic_source": traffic_src, "kernel": "batch_kernel",
+                    "traffic": traffic, "traffic_source": traffic_src, "kernel": kname,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
     roofline.update(bytes_per_flip=2 * n, batch_share_of_step=sum(batch_ms) / t_ms if world == 1 else None)
 

@@ -50,6 +50,8 @@ def build_variant(out: str, extra=()) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed")
+    with open(out + ".ptxas.log", "w") as f:
+        f.write(r.stdout + r.stderr)
     return out
 
 

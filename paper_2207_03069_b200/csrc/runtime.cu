@@ -15,14 +15,24 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dabs.h"
 #include "batch_kernel.cuh"
+#include "tmem_kernel.cuh"
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
 #include "jump_tc.cuh"
 #include "probe.cuh"
 
 using namespace dabs;
+
+// NVTX ranges around the C-ABI calls and the generation phases (header-only
+// nvtx3: no-ops unless a profiler injects itself)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 
@@ -54,6 +64,7 @@ struct dabs_ctx {
     int n = 0, n_pad = 0, nwp = 0, C = 0, NT = 0;
     int CL = 1;              // CTAs per search (2 = cluster tier)
     bool mw = false;
+    bool tm = false;         // TMEM tier (tm_batch_kernel): two 256-thread searches per SM, Delta in TMEM
     int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
     GaConst ga{};
     // device buffers
@@ -185,8 +196,10 @@ extern "C" int dabs_timing_read(unsigned long long* out)
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, g_tstat, sizeof(g_tstat));
     cudaMemcpyFromSymbol(out + 30, g_tstat2, sizeof(g_tstat2));
+    cudaMemcpyFromSymbol(out + 40, g_tstat3, sizeof(g_tstat3));
     static const unsigned long long zero[30] = {};
     cudaMemcpyToSymbol(g_tstat2, zero, sizeof(g_tstat2));
+    cudaMemcpyToSymbol(g_tstat3, zero, sizeof(g_tstat3));
     return (int)cudaMemcpyToSymbol(g_tstat, zero, sizeof(g_tstat));
 }
 #endif
@@ -225,7 +238,13 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
     default: return trace ? batch_kernel<8, 32, 1, true> : batch_kernel<8, 32, 1, false>;
     }
 }
-static BatchFn pick_batch(const dabs_ctx* c, bool trace) { return pick_batch(c->C, c->NT, c->CL, trace); }
+static BatchFn pick_batch(const dabs_ctx* c, bool trace)
+{
+    if (c->tm) return trace ? tm_batch_kernel<true> : tm_batch_kernel<false>;
+    return pick_batch(c->C, c->NT, c->CL, trace);
+}
+// threads per CTA of the generation schedule's batch kernel
+static int batch_threads(const dabs_ctx* c) { return c->tm ? TM_NT : c->NT; }
 
 using AsyncFn = void (*)(const AsyncArgs);
 static AsyncFn pick_async(int C, int NT, int CL)
@@ -249,9 +268,14 @@ static AsyncFn pick_async(int C, int NT, int CL)
 }
 
 // per CTA: its part of one W row + tabu counts (+ two copies of the sigma bytes, CTA tiers)
-static size_t row_smem(const dabs_ctx* c)
+static size_t row_smem_reg(const dabs_ctx* c)
 {
     return (size_t)(c->mw ? 5 : 3) * (c->n_pad / c->CL);
+}
+// the generation schedule's batch kernel: the TMEM tier keeps only the W row in dynamic smem
+static size_t row_smem(const dabs_ctx* c)
+{
+    return c->tm ? (size_t)2 * c->n_pad : row_smem_reg(c);
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
@@ -359,6 +383,10 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         int NT = 64;
         while (NT * 64 * c->CL < n) NT <<= 1;
         c->NT = NT;
+        // 16384 < n <= 32768: the TMEM tier for the generation schedule (DABS_TMEM=0: the
+        // 512-thread register tier, A/B).  The asynchronous schedule keeps the register tier.
+        const char* et = getenv("DABS_TMEM");
+        c->tm = c->CL == 1 && NT == 512 && !(et && et[0] == '0');
     }
     c->n_pad = c->NT * c->CL * c->C * 8;
     c->nwp = c->n_pad / 32;
@@ -369,7 +397,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     }
     {
         cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT, c->CL), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)std::max(row_smem(c), async_commit_smem((int)cfg.pool_capacity)));
+                                             (int)std::max(row_smem_reg(c), async_commit_smem((int)cfg.pool_capacity)));
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
     c->T = flip_factor(cfg.s_milli, n);
@@ -384,9 +412,9 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) != 0;
         if (one_wave)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT, c->CL), c->NT,
-                                                          std::max(row_smem(c), async_commit_smem((int)cfg.pool_capacity)));
+                                                          std::max(row_smem_reg(c), async_commit_smem((int)cfg.pool_capacity)));
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), c->NT, row_smem(c));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), batch_threads(c), row_smem(c));
         if (occ < 1) occ = 1;
         const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
         if (one_wave)
@@ -557,6 +585,7 @@ static dabs_status create_end(dabs_ctx* c)
 extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_config* cfg_in,
                                    dabs_ctx** out)
 {
+    NvtxRange nr_("dabs_create");
     if (!out) return fail(DABS_E_ARG, "out is NULL");
     *out = nullptr;
     if (!W_host) return fail(DABS_E_ARG, "W is NULL");
@@ -578,6 +607,7 @@ extern "C" dabs_status dabs_create(const int16_t* W_host, int32_t n, const dabs_
 extern "C" dabs_status dabs_create_csr(int32_t n, const int32_t* row_ptr, const int32_t* col, const int16_t* val,
                                        const int16_t* diag, const dabs_config* cfg_in, dabs_ctx** out)
 {
+    NvtxRange nr_("dabs_create_csr");
     if (!out) return fail(DABS_E_ARG, "out is NULL");
     *out = nullptr;
     if (!row_ptr || !diag) return fail(DABS_E_ARG, "row_ptr / diag is NULL");
@@ -696,7 +726,7 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     p.gen_ptr = gen_ptr;
     BatchFn fn = pick_batch(c, trace);
     if (c->CL == 1) {
-        fn<<<count, c->NT, row_smem(c), c->stream>>>(p);
+        fn<<<count, batch_threads(c), row_smem(c), c->stream>>>(p);
         c->launches++;
     } else {
         cudaLaunchConfig_t lc = {};
@@ -741,6 +771,7 @@ static dabs_status jump_start(dabs_ctx* c)
 // generation index from gen_d, copied in before every replay).
 static dabs_status enqueue_generation(dabs_ctx* c, bool graph)
 {
+    NvtxRange nr_("dabs.enqueue_generation");
     cudaStream_t st = c->stream;
     const uint32_t* genp = graph ? c->gen_d : nullptr;
     // inside a capture a plain event record only orders streams; the timing
@@ -809,6 +840,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
 {
     if (!c) return fail(DABS_E_ARG, "ctx is NULL");
     if (!c->ready) return fail(DABS_E_STATE, "dabs_generation before dabs_reset");
+    NvtxRange nr_("dabs_generation");
     CK(cudaSetDevice(c->dev));
     const auto t0 = std::chrono::steady_clock::now();
     cudaStream_t st = c->stream;
@@ -898,6 +930,7 @@ extern "C" dabs_status dabs_generation(dabs_ctx* c)
 extern "C" dabs_status dabs_run(dabs_ctx* c, uint64_t seed, uint64_t flip_budget, uint8_t* best_x,
                                 int64_t* best_e)
 {
+    NvtxRange nr_("dabs_run");
     dabs_status st = dabs_reset(c, seed);
     if (st != DABS_OK) return st;
     const auto t0 = std::chrono::steady_clock::now();
@@ -919,6 +952,7 @@ extern "C" dabs_status dabs_run(dabs_ctx* c, uint64_t seed, uint64_t flip_budget
 extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_budget, uint8_t* best_x,
                                       int64_t* best_e)
 {
+    NvtxRange nr_("dabs_run_async");
     if (!c) return fail(DABS_E_ARG, "ctx is NULL");
     if (c->cfg.world != 1) return fail(DABS_E_ARG, "the asynchronous schedule runs on one rank (world == 1)");
     if (c->cfg.restart_gens) return fail(DABS_E_ARG, "restart-on-merge is a generation-schedule option");
@@ -962,7 +996,7 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
     a.profile = getenv("DABS_ASYNC_PHASES") ? 1 : 0;
     CK(cudaEventRecord(c->ev[1], s0));
-    const size_t asmem = std::max(row_smem(c), async_commit_smem(c->cap));
+    const size_t asmem = std::max(row_smem_reg(c), async_commit_smem(c->cap));
     if (c->CL == 1) {
         pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, asmem, s0>>>(a);
         c->launches++;
@@ -1107,7 +1141,7 @@ extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
                 o->dispatch[a][g] += d[(p * N_ALG + a) * N_GEN + g];
                 o->inserted[a][g] += in[(p * N_ALG + a) * N_GEN + g];
             }
-    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = c->NT * c->CL; o->slots = c->slots; o->pools = c->P;
+    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = batch_threads(c) * c->CL; o->slots = c->slots; o->pools = c->P;
     o->T = c->T; o->B = c->B; o->cap = c->cap;
     o->kernel_launches = c->launches;
     return DABS_OK;

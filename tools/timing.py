@@ -16,7 +16,7 @@ NAMES = ["MaxMin", "CyclicMin", "RandomMin", "PositiveMin", "TwoNeighbor", "Stra
 
 
 def read(L):
-    out = (C.c_ulonglong * 40)()
+    out = (C.c_ulonglong * 56)()
     L.dabs_timing_read(out)
     a = np.array(out, dtype=np.float64)
     return a[:30].reshape(6, 5), a[30:]
@@ -51,6 +51,12 @@ def main():
         if nsel > 0:
             print("   MaxMin/PosMin sub-steps (cyc/flip): pass1 %.0f reduce1 %.0f thr %.0f count %.0f reduce2 %.0f "
                   "chunk %.0f wsel %.0f pickwait %.0f" % tuple(t2[:8] / nsel))
+        nfl = t[:, 4].sum()
+        t3 = t2[10:26]
+        if t3.sum() > 0 and nfl > 0:
+            print("   TMEM tier update per flip (cyc): " + "  ".join(
+                "piece%d ld %.0f wait %.0f upd %.0f" % (q, t3[3 * q] / nfl, t3[3 * q + 1] / nfl, t3[3 * q + 2] / nfl)
+                for q in range(4)) + "  st-drain %.0f" % (t3[12] / nfl))
         s.close()
 
 
