@@ -35,6 +35,7 @@ struct BatchParams {
     const int32_t* ptab;     // [T+1] RandomMin threshold p16(t) (R-8)
     const int32_t* rmax;     // [n] max_k |W_ik|: bounds how far any Delta can fall per flip
     double invT3;            // 1 / T^3 (MaxMin span estimate, corrected exactly)
+    const uint64_t* mtab;    // [T+1] floor(2^64 (T-t)^3 / T^3) (MaxMin span estimate, TMEM tier)
     int n, n_pad, nwp;       // nwp = n_pad / 32 words per bit vector
     int T, B, tabu;
     uint64_t seed;

@@ -73,6 +73,7 @@ struct dabs_ctx {
     int32_t* diag = nullptr;
     int32_t* rmax = nullptr;
     int32_t *wtab = nullptr, *ptab = nullptr;
+    uint64_t* mtab = nullptr;   // MaxMin: floor(2^64 (T-t)^3 / T^3) per step t (R-6; TMEM tier)
     uint32_t* X = nullptr;
     int32_t* delta = nullptr;
     int64_t* E = nullptr;
@@ -283,6 +284,7 @@ static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     BatchParams p{};
     p.W = c->W; p.wtab = c->wtab; p.ptab = c->ptab; p.rmax = c->rmax;
     p.invT3 = 1.0 / ((double)c->T * (double)c->T * (double)c->T);
+    p.mtab = c->mtab;
     p.n = c->n; p.n_pad = c->n_pad; p.nwp = c->nwp;
     p.T = c->T; p.B = c->B; p.tabu = c->tabu;
     p.seed = seed; p.gen = gen;
@@ -500,8 +502,11 @@ static dabs_status create_end(dabs_ctx* c)
     // ---- schedule tables for CyclicMin (R-7) and RandomMin (R-8)
     {
         std::vector<int32_t> wt(c->T + 1), pt(c->T + 1);
+        std::vector<uint64_t> mt(c->T + 1);
         const unsigned __int128 T3 = (unsigned __int128)c->T * c->T * c->T;
         for (int t = 0; t <= c->T; t++) {
+            const unsigned __int128 u = (unsigned __int128)(c->T - t);
+            mt[t] = t == 0 ? ~0ull : (uint64_t)(((u * u * u) << 64) / T3);   // u^3 < T^3: below 2^64
             const unsigned __int128 t3 = (unsigned __int128)t * t * t;
             uint64_t w = (uint64_t)(((unsigned __int128)n * t3 + T3 - 1) / T3);
             const uint64_t cmin = n < 32 ? (uint64_t)n : 32u;
@@ -518,6 +523,8 @@ static dabs_status create_end(dabs_ctx* c)
         if ((st = dalloc(c, &c->ptab, c->T + 1)) != DABS_OK) return bail(st);
         cudaMemcpyAsync(c->wtab, wt.data(), 4 * wt.size(), cudaMemcpyHostToDevice, c->stream);
         cudaMemcpyAsync(c->ptab, pt.data(), 4 * pt.size(), cudaMemcpyHostToDevice, c->stream);
+        if ((st = dalloc(c, &c->mtab, c->T + 1)) != DABS_OK) return bail(st);
+        cudaMemcpyAsync(c->mtab, mt.data(), 8 * mt.size(), cudaMemcpyHostToDevice, c->stream);
         if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(DABS_E_CUDA, "tables"));
     }
 

@@ -61,12 +61,11 @@ __device__ __forceinline__ void tm_ld32(uint32_t ta, int32_t (&v)[32])
         : DABS_R8(v, 0), DABS_R8(v, 8), DABS_R8(v, 16), DABS_R8(v, 24)
         : "r"(ta));
 }
-// wait for this thread's TMEM loads; the "+r" operands keep every use of v after it
-__device__ __forceinline__ void tm_wait_ld32(int32_t (&v)[32])
+// wait for this thread's TMEM loads (ptxas tracks the LDTM destinations on a
+// scoreboard; the wait orders the load against later TMEM stores of the thread)
+__device__ __forceinline__ void tm_wait_ld32(int32_t (&)[32])
 {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : DABS_W8(v, 0), DABS_W8(v, 8), DABS_W8(v, 16), DABS_W8(v, 24)
-                 :
-                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tm_st32(uint32_t ta, const int32_t (&v)[32])
 {
@@ -82,9 +81,9 @@ __device__ __forceinline__ void tm_ld16(uint32_t ta, int32_t (&v)[16])
                  : DABS_R8(v, 0), DABS_R8(v, 8)
                  : "r"(ta));
 }
-__device__ __forceinline__ void tm_wait_ld16(int32_t (&v)[16])
+__device__ __forceinline__ void tm_wait_ld16(int32_t (&)[16])
 {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : DABS_W8(v, 0), DABS_W8(v, 8) : : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tm_st16(uint32_t ta, const int32_t (&v)[16])
 {
@@ -627,9 +626,12 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
             }
             uint32_t u;
             if (algo == ALG_MAXMIN) {
+                // span = floor((hi - lo) u^3 / T^3) exactly (R-6): the estimate from the
+                // step's 64-bit fraction is floor or floor - 1; one remainder test fixes it
                 const uint64_t uu = (uint64_t)(T - tt);
-                const uint64_t span = muldiv_floor((uint64_t)((int64_t)v[2] - v[1]), uu * uu * uu,
-                                                   (uint64_t)T * T * T, p.invT3);
+                const uint64_t a = (uint64_t)((int64_t)v[2] - v[1]), f = uu * uu * uu, qd = (uint64_t)T * T * T;
+                uint64_t span = __umul64hi(a, p.mtab[tt]);
+                if (a * f - span * qd >= qd) span++;
                 thr = (int)((int64_t)v[1] + (int64_t)(((unsigned __int128)r.x * (span + 1)) >> 32));
                 u = r.y;
             } else {
@@ -641,19 +643,29 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
             uint32_t pk[CW];
 #pragma unroll
             for (int w = 0; w < CW; w++) pk[w] = 0;
+            {
+                // x16 half-pieces (chunks c0, c0 + 1), the next load in flight
+                auto count16 = [&](const int32_t (&v16)[16], const int c0) {
 #pragma unroll
-            for (int q = 0; q < NP; q++) {
-                int32_t v32[32];
-                tm_ld32(tw + 32 * q, v32);
-                tm_wait_ld32(v32);
+                    for (int cc = 0; cc < 2; cc++) {
+                        const int c = c0 + cc;
+                        uint32_t byte = 0;
 #pragma unroll
-                for (int cc = 0; cc < CPP; cc++) {
-                    const int c = q * CPP + cc;
-                    uint32_t byte = 0;
+                        for (int e = 0; e < 8; e++) byte |= (uint32_t)(v16[8 * cc + e] <= thr) << e;
+                        byte &= mbyte(EL, c);
+                        pk[c >> 1] += (uint32_t)__popc(byte) << (16 * (c & 1));
+                    }
+                };
+                int32_t va[16], vb2[16];
+                tm_ld16(tw, va);
 #pragma unroll
-                    for (int e = 0; e < 8; e++) byte |= (uint32_t)(v32[8 * cc + e] <= thr) << e;
-                    byte &= mbyte(EL, c);
-                    pk[c >> 1] += (uint32_t)__popc(byte) << (16 * (c & 1));
+                for (int q = 0; q < NP; q++) {
+                    tm_wait_ld16(va);
+                    tm_ld16(tw + 32 * q + 16, vb2);
+                    count16(va, 4 * q);
+                    tm_wait_ld16(vb2);
+                    if (q + 1 < NP) tm_ld16(tw + 32 * q + 32, va);
+                    count16(vb2, 4 * q + 2);
                 }
             }
             DABS_TS(3);
