@@ -417,7 +417,7 @@ __device__ __forceinline__ bool async_commit(const AsyncArgs& a, int s, uint32_t
 // register budget of the batch kernel of the same tier: warp tier C <= 4 -> 16
 // CTAs per SM (128 registers), C = 8 -> 12; CTA tiers unconstrained
 template <int C, int NTT, int CL>
-__global__ void __launch_bounds__(NTT, NTT == 32 ? (C <= 4 ? 16 : 12) : 0) async_kernel(const AsyncArgs a)
+__global__ void __launch_bounds__(NTT, NTT == 32 ? 16 : 0) async_kernel(const AsyncArgs a)
 {
     const int s = (int)blockIdx.x / CL;
     const unsigned long long t_start = globaltimer();

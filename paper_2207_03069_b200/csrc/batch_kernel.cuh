@@ -1238,8 +1238,24 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
     }
 }
 
+// Warp tier: minimum resident searches per SM, i.e. a register cap.  The tier
+// is issue/latency bound, more resident warps beat the few spills the cap
+// costs (A/B on B200, tools/gpu_ab_libs.sh: uncapped 167 / 128 registers ->
+// 128 / 80: K2000s +13 %, TSP32 +7 %, GS800 +6 % flips/s).
+#ifndef DABS_MINB8
+#define DABS_MINB8 16   // C = 8 (1024 < n <= 2048): 128 registers, 16 searches per SM
+#endif
+#ifndef DABS_MINB4
+#define DABS_MINB4 24   // C = 4 (512 < n <= 1024): 80 registers, 24 searches per SM
+#endif
+template <int C, int NTT, int CL>
+constexpr int batch_min_blocks()
+{
+    return (CL == 2 && NTT <= 256) ? 2 : (NTT == 32 && C == 8) ? DABS_MINB8 : (NTT == 32 && C == 4) ? DABS_MINB4 : 0;
+}
+
 template <int C, int NTT, int CL, bool TRACE>
-__global__ void __launch_bounds__(NTT, (CL == 2 && NTT <= 256) ? 2 : 0) batch_kernel(const BatchParams p)
+__global__ void __launch_bounds__(NTT, batch_min_blocks<C, NTT, CL>()) batch_kernel(const BatchParams p)
 {
     const int sidx = (int)blockIdx.x / CL;
     const int s = p.order ? p.order[sidx] : p.slot0 + sidx;

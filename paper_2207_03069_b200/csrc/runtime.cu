@@ -395,6 +395,11 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
     for (int tr = 0; tr < 2; tr++) {
         cudaError_t e = cudaFuncSetAttribute(pick_batch(c, tr != 0),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
+        // TMEM tier: the full shared-memory carveout, so two searches fit per SM
+        // (and the occupancy query below sees them)
+        if (e == cudaSuccess && c->tm)
+            e = cudaFuncSetAttribute(pick_batch(c, tr != 0), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
     {
