@@ -422,6 +422,11 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
                                                           std::max(row_smem_reg(c), async_commit_smem((int)cfg.pool_capacity)));
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), batch_threads(c), row_smem(c));
+        if (getenv("DABS_DEBUG_OCC")) fprintf(stderr, "dabs: occupancy %d CTAs/SM (tier NT=%d C=%d CL=%d tm=%d)\n", occ,
+                                             batch_threads(c), c->C, c->CL, (int)c->tm);
+        // the TMEM tier is built for two co-resident searches per SM (ncu: 16
+        // active warps per SM); the occupancy query reports one for it
+        if (c->tm && !one_wave && occ < 2) occ = 2;
         if (occ < 1) occ = 1;
         const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
         if (one_wave)
@@ -429,11 +434,17 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         else {
             // several waves per generation: batch lengths differ (TwoNeighbor runs
             // 2n-1 main flips), more waves let the block scheduler balance them.
-            // Four waves.  More waves shorten the last wave's idle tail by only
+            // Four waves for the register tiers: more waves shorten the last wave's idle tail by only
             // 1-3 % at a fixed algorithm (tools/waves_fixed_algo.py); the larger
             // flips/s changes seen with more slots per generation come from the
             // adaptive algorithm mix, not from the kernels (DESIGN 5)
-            const int waves = 4;
+            // The TMEM tier (two searches per SM, long R32K batches) loses more to
+            // the last wave's tail: 4 -> 8 -> 16 waves measured 0.661 -> 0.686 ->
+            // 0.718 of the HBM roofline with the adaptive mix and +6-8 % for every
+            // fixed rule (tools/gpu_waves.sh), at ~2.3 s per generation.
+            // DABS_WAVES overrides (A/B).
+            const char* ewv = getenv("DABS_WAVES");
+            const int waves = ewv ? std::max(1, atoi(ewv)) : (c->tm ? 16 : 4);
             c->S = (waves * conc + c->P - 1) / c->P;
         }
     }
