@@ -61,6 +61,12 @@ struct BatchParams {
     int64_t tr_cap;
 };
 
+// warp tier: sigma words from a 256-entry table instead of 16 sign registers
+// (A/B on B200, tools/gpu_ab_warp.sh: K2000s +4.7 %, TSP32 +4.9 %, GS800 +4.0 %)
+#ifndef DABS_WARP_LUT
+#define DABS_WARP_LUT 1
+#endif
+
 #ifndef DABS_NP_MAX
 #define DABS_NP_MAX 4   // W-row pieces (one mbarrier each) per flip in the CTA tiers (A/B: -DDABS_NP_MAX=8)
 #endif
@@ -445,11 +451,28 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
     // memory, [2][ceil(C/2)][NT] uint4 (16 bytes = two chunks per thread,
     // conflict-free), copy 0 as is for sigma(x_i) = +1 and copy 1 negated for
     // sigma(x_i) = -1, so the update needs no per-word negation.
-    uint32_t sg[MW ? 1 : EPT / 4];
+    // DABS_WARP_LUT: the warp tier takes the four IDP.2A sign words of a chunk
+    // from a 256-entry table indexed by the chunk's 8 x bits (as the TMEM tier)
+    // instead of keeping sigma bytes in 16 registers
+    constexpr bool WLUT = !MW && DABS_WARP_LUT;
+    __shared__ uint4 lutw_s[WLUT ? 256 : 1];
+    if constexpr (WLUT) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t v = (uint32_t)(j * 32 + t);
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; h++)
+                w[h] = (((v >> (2 * h)) & 1u) ? 0x01u : 0xFFu) | ((((v >> (2 * h + 1)) & 1u) ? 0x01u : 0xFFu) << 24);
+            lutw_s[v] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        __syncwarp();
+    }
+    uint32_t sg[(MW || WLUT) ? 1 : EPT / 4];
     uint4* sgs = reinterpret_cast<uint4*>(dyn_smem + 3 * nl);
     constexpr int SGC = ((C + 1) / 2) << lgNT;   // uint4s per copy
 #pragma unroll
-    for (int g = 0; g < EPT / 4; g++) {
+    for (int g = 0; g < ((MW || !WLUT) ? EPT / 4 : 0); g++) {
         uint32_t w = 0;
 #pragma unroll
         for (int j = 0; j < 4; j++) w |= (((xb >> (4 * g + j)) & 1) ? 0x01u : 0xFFu) << (8 * j);
@@ -1107,7 +1130,8 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
                     b8[off] ^= 0xFEu;
                     b8[off + SGC * 16] ^= 0xFEu;
                 } else {
-                    owner_flip(d, sg, kk);       // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
+                    if constexpr (WLUT) neg_at(d, kk);
+                    else owner_flip(d, sg, kk);  // Eq.(5); W_ii = 0, so the update leaves Delta_i alone
                 }
                 xb ^= ONE << kk;
                 bdiff ^= ONE << kk;
@@ -1172,9 +1196,15 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
                 for (int cc = 0; cc < CPP; cc++) {
                     const int c = qq * CPP + cc;
                     // Eq.(4) as above; B holds (s_k0, 0, 0, s_k1) as int8x4, byte-permuted here
-                    const uint32_t g0 = sg[2 * c] ^ cmask, g1 = sg[2 * c + 1] ^ cmask;
-                    const uint32_t B0 = __byte_perm(g0, 0, 0x1440), B1 = __byte_perm(g0, 0, 0x3442);
-                    const uint32_t B2 = __byte_perm(g1, 0, 0x1440), B3 = __byte_perm(g1, 0, 0x3442);
+                    uint32_t B0, B1, B2, B3;
+                    if constexpr (WLUT) {
+                        const uint4 Bq = lutw_s[(uint32_t)((xb >> (8 * c)) & 0xFFu) ^ (cmask ? 0xFFu : 0u)];
+                        B0 = Bq.x; B1 = Bq.y; B2 = Bq.z; B3 = Bq.w;
+                    } else {
+                        const uint32_t g0 = sg[2 * c] ^ cmask, g1 = sg[2 * c + 1] ^ cmask;
+                        B0 = __byte_perm(g0, 0, 0x1440); B1 = __byte_perm(g0, 0, 0x3442);
+                        B2 = __byte_perm(g1, 0, 0x1440); B3 = __byte_perm(g1, 0, 0x3442);
+                    }
                     d[8 * c + 0] = __dp2a_lo((int)rw[cc].x, (int)B0, d[8 * c + 0]);
                     d[8 * c + 1] = __dp2a_hi((int)rw[cc].x, (int)B0, d[8 * c + 1]);
                     d[8 * c + 2] = __dp2a_lo((int)rw[cc].y, (int)B1, d[8 * c + 2]);

@@ -442,6 +442,9 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
             // the last wave's tail: 4 -> 8 -> 16 waves measured 0.661 -> 0.686 ->
             // 0.718 of the HBM roofline with the adaptive mix and +6-8 % for every
             // fixed rule (tools/gpu_waves.sh), at ~2.3 s per generation.
+            // The warp tier keeps four: 16 waves measured K2000s +17 %, TSP32 +5 %,
+            // GS800 +9 % flips/s but 54 ms generations at TSP32 (the pools, and
+            // the time to target, move once per generation; tools/gpu_ab_warp.sh).
             // DABS_WAVES overrides (A/B).
             const char* ewv = getenv("DABS_WAVES");
             const int waves = ewv ? std::max(1, atoi(ewv)) : (c->tm ? 16 : 4);

@@ -3,9 +3,11 @@
     compute-sanitizer --tool racecheck python tools/sanitize_case.py async
 cases: async   -- dabs_run_async, n = 96, 2 pools, one wave (ticket locks, pool merge)
        cluster -- generations on the forced 2-CTA cluster tier, n = 5000 (DSMEM swaps, mbarriers)
-       cta     -- the 512-thread CTA tier (R32K's), n = 16385 (TMA rows, CTA exchange): a batch
-                  to a local minimum, then a short checked batch (sanitize only the 2nd batch_kernel
-                  launch: --kernel-name kns=batch_kernel --launch-skip 1 --launch-count 1)
+       cta     -- R32K's tier, n = 16385: the TMEM tier (tm_batch_kernel: TMEM alloc, tcgen05.ld/st,
+                  TMA rows, CTA exchange): a batch to a local minimum, then a short checked batch
+                  (sanitize only the 2nd launch: --kernel-name kns=batch_kernel --launch-skip 1
+                  --launch-count 1)
+       ctareg  -- the same on the 512-thread register tier (DABS_TMEM=0, kept by the async schedule)
        warp    -- generations on the warp tier, n = 1000
 Each case also checks its result against the CPU oracle (so a run that the
 tool perturbs into a wrong answer fails loudly)."""
@@ -21,6 +23,9 @@ def main(case):
     from paper_2207_03069_b200 import Solver, workloads as wl
     if case == "cluster":
         os.environ["DABS_CLUSTER"] = "1"
+    if case == "ctareg":
+        os.environ["DABS_TMEM"] = "0"
+        case = "cta"
     n = {"async": 96, "cluster": 5000, "cta": 16385, "warp": 1000}[case]
     U = wl.random_dense(n, seed=3, lo=-200, hi=200)
     if case == "async":

@@ -36,8 +36,8 @@ def main():
                 pass
     dram = float(d["dram__bytes_read.sum"]) * UNIT[u["dram__bytes_read.sum"]] + \
         float(d["dram__bytes_write.sum"]) * UNIT[u["dram__bytes_write.sum"]]
-    dur_s = float(d["gpu__time_duration.sum"]) * {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3}.get(
-        u["gpu__time_duration.sum"], 1e-9)
+    dur_s = float(d["gpu__time_duration.sum"]) * {"s": 1.0, "second": 1.0, "ms": 1e-3, "us": 1e-6, "usecond": 1e-6,
+                                                   "msecond": 1e-3}.get(u["gpu__time_duration.sum"], 1e-9)
     l2 = float(d["lts__t_bytes.sum"]) * UNIT.get(u.get("lts__t_bytes.sum", "byte"), 1.0) if d.get("lts__t_bytes.sum") else None
     summary = {
         "workload": workload, "kernel": d.get("Kernel Name"), "report": rep,
