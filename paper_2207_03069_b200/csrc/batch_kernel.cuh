@@ -43,6 +43,7 @@ struct BatchParams {
     const uint32_t* gen_ptr; // graph replays: the generation index in device memory (else gen)
     uint32_t slot_base;      // global id of local slot 0
     int slot0;               // first local slot of this launch (blockIdx.x offset)
+    int count;               // searches in this launch (the TMEM warp tier packs 4 per CTA)
     const int32_t* order;    // optional launch order of the slots (longest batches first)
     uint32_t* X;             // [slots][nwp]   persistent x (R-14)
     int32_t* delta;          // [slots][n_pad] persistent Delta (pads = INT32_MAX)
@@ -586,13 +587,7 @@ __device__ __forceinline__ void batch_body(const BatchParams& p, const int s, co
 #pragma unroll
         for (int c = 0; c < C; c++) {
             const uint32_t j0 = (uint32_t)(((c << lgNTG) + tq) << 2);   // first pair of the chunk
-            uint32_t byte = 0;
-#pragma unroll
-            for (int h = 0; h < 4; h++) {
-                const uint32_t x = lowbias32(K + (j0 + h) * 0x9E3779B9u);
-                byte |= ((uint32_t)((x & 0xFFFFu) < p16) | ((uint32_t)((x >> 16) < p16) << 1)) << (2 * h);
-            }
-            cand |= (bits_t)byte << (8 * c);
+            cand |= (bits_t)randmin_byte(K, j0, p16) << (8 * c);
         }
         return cand;
     };

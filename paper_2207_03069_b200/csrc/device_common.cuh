@@ -48,6 +48,18 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x)
     return x;
 }
 
+// RandomMin candidate bits of 4 consecutive bit pairs j0..j0+3 (R-8): bit 2h / 2h+1
+// = (low / high 16 bits of lowbias32(K + (j0 + h) * 0x9E3779B9)) < p16, p16 < 65536.
+// Both halves are compared at once with the SIMD-within-register __vsetltu2.
+__device__ __forceinline__ uint32_t randmin_byte(uint32_t K, uint32_t j0, uint32_t p16)
+{
+    const uint32_t P = p16 | (p16 << 16);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int h = 0; h < 4; h++) acc |= __vsetltu2(lowbias32(K + (j0 + h) * 0x9E3779B9u), P) << (2 * h);
+    return (acc & 0x55u) | ((acc >> 15) & 0xAAu);
+}
+
 // floor(u * m / 2^32)  (R-15)
 __device__ __forceinline__ uint32_t pick_u(uint32_t u, uint32_t m)
 {

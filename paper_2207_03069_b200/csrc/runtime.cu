@@ -20,6 +20,7 @@
 #include "../../include/dabs.h"
 #include "batch_kernel.cuh"
 #include "tmem_kernel.cuh"
+#include "tmw_kernel.cuh"
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
 #include "jump_tc.cuh"
@@ -65,6 +66,7 @@ struct dabs_ctx {
     int CL = 1;              // CTAs per search (2 = cluster tier)
     bool mw = false;
     bool tm = false;         // TMEM tier (tm_batch_kernel): two 256-thread searches per SM, Delta in TMEM
+    bool tmw = false;        // TMEM warp tier (tmw_batch_kernel): 4 warp-searches per CTA, Delta in TMEM
     int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
     GaConst ga{};
     // device buffers
@@ -242,10 +244,16 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
 static BatchFn pick_batch(const dabs_ctx* c, bool trace)
 {
     if (c->tm) return trace ? tm_batch_kernel<true> : tm_batch_kernel<false>;
+    if (c->tmw) {
+        if (c->C == 8) return trace ? tmw_batch_kernel<8, true> : tmw_batch_kernel<8, false>;
+        return trace ? tmw_batch_kernel<4, true> : tmw_batch_kernel<4, false>;
+    }
     return pick_batch(c->C, c->NT, c->CL, trace);
 }
 // threads per CTA of the generation schedule's batch kernel
-static int batch_threads(const dabs_ctx* c) { return c->tm ? TM_NT : c->NT; }
+static int batch_threads(const dabs_ctx* c) { return c->tm ? TM_NT : c->tmw ? 32 * TMW_SPC : c->NT; }
+// searches per CTA of the generation schedule's batch kernel
+static int batch_spc(const dabs_ctx* c) { return c->tmw ? TMW_SPC : 1; }
 
 using AsyncFn = void (*)(const AsyncArgs);
 static AsyncFn pick_async(int C, int NT, int CL)
@@ -276,7 +284,7 @@ static size_t row_smem_reg(const dabs_ctx* c)
 // the generation schedule's batch kernel: the TMEM tier keeps only the W row in dynamic smem
 static size_t row_smem(const dabs_ctx* c)
 {
-    return c->tm ? (size_t)2 * c->n_pad : row_smem_reg(c);
+    return c->tm ? (size_t)2 * c->n_pad : c->tmw ? (size_t)2 * c->n_pad * TMW_SPC : row_smem_reg(c);
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
@@ -290,6 +298,7 @@ static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     p.seed = seed; p.gen = gen;
     p.slot_base = (uint32_t)(c->cfg.rank * c->slots);
     p.slot0 = slot0;
+    p.count = 0;
     p.X = c->X; p.delta = c->delta; p.E = c->E; p.ring = c->ring;
     p.D = c->D; p.algo = c->palgo;
     p.best = c->best; p.ebest = c->ebest; p.flips = c->flips;
@@ -374,6 +383,12 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         int C = 1;
         while (C * 256 < n) C <<= 1;
         c->C = C;
+        // 512 < n <= 2048, DABS_TMW=1 (A/B, off by default): the TMEM warp tier,
+        // 32 searches per SM with Delta in TMEM.  Measured break-even at K2000s
+        // (7.34e8 vs 7.41e8 flips/s: MaxMin/PositiveMin +13/+25 %, RandomMin
+        // -9 %) and -19 % at TSP32 (tools/gpu_tmw.sh, gpu_tmw2.sh; DESIGN 9)
+        const char* ew = getenv("DABS_TMW");
+        c->tmw = C >= 4 && ew && ew[0] == '1';
     } else {
         // one CTA of NT threads x 64 elements (n <= 32768), else a cluster of
         // two such CTAs (n <= 65536).  DABS_CLUSTER=1 forces the
@@ -397,7 +412,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem(c));
         // TMEM tier: the full shared-memory carveout, so two searches fit per SM
         // (and the occupancy query below sees them)
-        if (e == cudaSuccess && c->tm)
+        if (e == cudaSuccess && (c->tm || c->tmw))
             e = cudaFuncSetAttribute(pick_batch(c, tr != 0), cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
@@ -427,8 +442,10 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         // the TMEM tier is built for two co-resident searches per SM (ncu: 16
         // active warps per SM); the occupancy query reports one for it
         if (c->tm && !one_wave && occ < 2) occ = 2;
+        if (c->tmw && !one_wave && occ < 8) occ = 8;   // 8 CTAs x 4 searches: the TMEM columns and 64 registers
         if (occ < 1) occ = 1;
-        const int conc = std::max(1, prop.multiProcessorCount * occ / c->CL);   // concurrent searches
+        // concurrent searches (the TMEM warp tier packs 4 per CTA)
+        const int conc = std::max(1, prop.multiProcessorCount * occ * (one_wave ? 1 : batch_spc(c)) / c->CL);
         if (one_wave)
             c->S = std::max(1, conc / c->P);    // persistent CTAs of the asynchronous schedule, all resident
         else {
@@ -750,9 +767,11 @@ static dabs_status launch_batch(dabs_ctx* c, uint64_t seed, uint32_t gen, int sl
     BatchParams p = batch_params(c, seed, gen, slot0);
     p.order = order;
     p.gen_ptr = gen_ptr;
+    p.count = count;
     BatchFn fn = pick_batch(c, trace);
     if (c->CL == 1) {
-        fn<<<count, batch_threads(c), row_smem(c), c->stream>>>(p);
+        const int spc = batch_spc(c);
+        fn<<<(count + spc - 1) / spc, batch_threads(c), row_smem(c), c->stream>>>(p);
         c->launches++;
     } else {
         cudaLaunchConfig_t lc = {};
@@ -1167,7 +1186,7 @@ extern "C" dabs_status dabs_get_stats(const dabs_ctx* c, dabs_stats* o)
                 o->dispatch[a][g] += d[(p * N_ALG + a) * N_GEN + g];
                 o->inserted[a][g] += in[(p * N_ALG + a) * N_GEN + g];
             }
-    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = batch_threads(c) * c->CL; o->slots = c->slots; o->pools = c->P;
+    o->n = c->n; o->n_pad = c->n_pad; o->threads_per_search = batch_threads(c) / batch_spc(c) * c->CL; o->slots = c->slots; o->pools = c->P;
     o->T = c->T; o->B = c->B; o->cap = c->cap;
     o->kernel_launches = c->launches;
     return DABS_OK;

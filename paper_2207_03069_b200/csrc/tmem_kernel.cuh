@@ -302,14 +302,7 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
     // RandomMin candidates of chunk c (R-8)
     auto cand_byte = [&](int c, uint32_t K, uint32_t p16) -> uint32_t {
         if (p16 >= 65536u) return mbyte(vb, c);
-        const uint32_t j0 = (uint32_t)(((c << lgNT) + t) << 2);
-        uint32_t byte = 0;
-#pragma unroll
-        for (int h = 0; h < 4; h++) {
-            const uint32_t x = lowbias32(K + (j0 + h) * 0x9E3779B9u);
-            byte |= ((uint32_t)((x & 0xFFFFu) < p16) | ((uint32_t)((x >> 16) < p16) << 1)) << (2 * h);
-        }
-        return byte;
+        return randmin_byte(K, (uint32_t)(((c << lgNT) + t) << 2), p16);
     };
 
 #ifdef DABS_TIMING

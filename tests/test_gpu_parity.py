@@ -107,6 +107,23 @@ def test_batch_parity_cluster_forced(orc, lib, cluster_tier, n):
     solver.close()
 
 
+@pytest.mark.parametrize("n", [513, 1000, 1024, 1500, 2048])
+def test_batch_parity_tmem_warp_tier(orc, lib, monkeypatch, n):
+    """The TMEM warp tier (DABS_TMW=1: 4 warp-searches per CTA, Delta in tensor
+    memory; an A/B variant, off by default): every rule per flip, same bar."""
+    monkeypatch.setenv("DABS_TMW", "1")
+    rng = np.random.default_rng(3000 + n)
+    U = rand_upper(rng, n, -32767, 32767)
+    solver = lib.Solver(U, s_milli=150, b_milli=1500, tabu=8, pools=1, slots=2)
+    assert solver.stats().threads_per_search == 32
+    for algo in ALGS:
+        st = random_state(orc, rng, U, n_ring=5)
+        D = rng.integers(0, 2, n).astype(np.uint8)
+        compare_batch(orc, solver, U, st, D, algo, int(rng.integers(0, 2**63)), gslot=1,
+                      gen=int(rng.integers(0, 1000)), T=solver.T, B=solver.B, tabu=8)
+    solver.close()
+
+
 @pytest.fixture(scope="module")
 def r64k():
     from paper_2207_03069_b200 import workloads as wl
