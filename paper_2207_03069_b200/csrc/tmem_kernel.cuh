@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
     __shared__ int32_t sel_s[4];
     __shared__ uint4 lut_s[256];      // sigma bytes of 8 elements as the four IDP.2A B words
     __shared__ M128 pm_s[3][NT];      // [0] D bits, [1] M2, [2] BEST xor X
+    __shared__ int32_t cmin_s[C][NT]; // MaxMin / PositiveMin: per-chunk minima of the last scan
 
     // ---------------- TMEM: 256 columns for this search
     if (wid == 0) tm_alloc(&tbase_s, TM_COLS);
@@ -414,6 +415,7 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
             }
         } else if constexpr (md == SM_MM) {
             tg = min(tg, mn);
+            cmin_s[c][t] = mn;          // the counting pass skips chunks whose minimum exceeds thr
             if (mb == 0xFFu) {
                 const int mx = max(max(max(dc[0], dc[1]), max(dc[2], dc[3])), max(max(dc[4], dc[5]), max(dc[6], dc[7])));
                 a1 = min(a1, mn);
@@ -425,10 +427,16 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
             }
         } else {   // SM_PM
             tg = min(tg, mn);
+            cmin_s[c][t] = mn;
             unsigned q = 0xFFFFFFFFu;
+            if (mb == 0xFFu) {          // no tabu bit, no padding in the chunk (the common case)
 #pragma unroll
-            for (int e = 0; e < 8; e++)
-                if ((mb >> e) & 1u) q = min(q, (unsigned)(dc[e] - 1));
+                for (int e = 0; e < 8; e++) q = min(q, (unsigned)(dc[e] - 1));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; e++)
+                    if ((mb >> e) & 1u) q = min(q, (unsigned)(dc[e] - 1));
+            }
             tp = min(tp, q);
         }
     };
@@ -649,16 +657,18 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
                         pk[c >> 1] += (uint32_t)__popc(byte) << (16 * (c & 1));
                     }
                 };
-                int32_t va[16], vb2[16];
-                tm_ld16(tw, va);
+                // a half-piece whose chunk minima (all elements, from the scan) exceed
+                // thr in every lane of the warp holds no candidate: skip its TMEM
+                // load (PositiveMin: thr = the least positive gain, so most are skipped)
 #pragma unroll
-                for (int q = 0; q < NP; q++) {
-                    tm_wait_ld16(va);
-                    tm_ld16(tw + 32 * q + 16, vb2);
-                    count16(va, 4 * q);
-                    tm_wait_ld16(vb2);
-                    if (q + 1 < NP) tm_ld16(tw + 32 * q + 32, va);
-                    count16(vb2, 4 * q + 2);
+                for (int hp = 0; hp < C / 2; hp++) {
+                    const bool need = (cmin_s[2 * hp][t] <= thr) || (cmin_s[2 * hp + 1][t] <= thr);
+                    if (__any_sync(FULL, need)) {
+                        int32_t v16[16];
+                        tm_ld16(tw + 16 * hp, v16);
+                        tm_wait_ld16(v16);
+                        count16(v16, 2 * hp);
+                    }
                 }
             }
             DABS_TS(3);

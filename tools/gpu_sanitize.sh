@@ -2,7 +2,7 @@
 # search tier and the asynchronous schedule
 mkdir -p gpurun_out/sanitize
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-for case in ${CASES:-async cluster cta ctareg warp}; do
+for case in ${CASES:-async cluster cta ctareg warp tmw}; do
   for tool in memcheck racecheck synccheck; do
     flt=""; [ "$case" = cta -o "$case" = ctareg ] && flt="--kernel-name kns=batch_kernel --launch-skip 1 --launch-count 1"
     timeout 900 compute-sanitizer --tool $tool --print-limit 20 $flt \

@@ -8,6 +8,7 @@ cases: async   -- dabs_run_async, n = 96, 2 pools, one wave (ticket locks, pool 
                   (sanitize only the 2nd launch: --kernel-name kns=batch_kernel --launch-skip 1
                   --launch-count 1)
        ctareg  -- the same on the 512-thread register tier (DABS_TMEM=0, kept by the async schedule)
+       tmw     -- generations on the TMEM warp tier (DABS_TMW=1), n = 1000
        warp    -- generations on the warp tier, n = 1000
 Each case also checks its result against the CPU oracle (so a run that the
 tool perturbs into a wrong answer fails loudly)."""
@@ -26,6 +27,9 @@ def main(case):
     if case == "ctareg":
         os.environ["DABS_TMEM"] = "0"
         case = "cta"
+    if case == "tmw":
+        os.environ["DABS_TMW"] = "1"
+        case = "warp"
     n = {"async": 96, "cluster": 5000, "cta": 16385, "warp": 1000}[case]
     U = wl.random_dense(n, seed=3, lo=-200, hi=200)
     if case == "async":
