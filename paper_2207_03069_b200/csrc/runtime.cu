@@ -386,7 +386,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         // 512 < n <= 2048, DABS_TMW=1 (A/B, off by default): the TMEM warp tier,
         // 32 searches per SM with Delta in TMEM.  Measured break-even at K2000s
         // (7.34e8 vs 7.41e8 flips/s: MaxMin/PositiveMin +13/+25 %, RandomMin
-        // -9 %) and -19 % at TSP32 (tools/gpu_tmw.sh, gpu_tmw2.sh; DESIGN 9)
+        // -9 %) and -19 % at TSP32 (tools/gpu_tmw.sh; DESIGN 9)
         const char* ew = getenv("DABS_TMW");
         c->tmw = C >= 4 && ew && ew[0] == '1';
     } else {
