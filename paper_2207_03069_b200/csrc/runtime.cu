@@ -23,6 +23,7 @@
 #include "tmw_kernel.cuh"
 #include "ga_pool_kernels.cuh"
 #include "async_kernel.cuh"
+#include "tmem_async.cuh"
 #include "jump_tc.cuh"
 #include "probe.cuh"
 
@@ -66,6 +67,7 @@ struct dabs_ctx {
     int CL = 1;              // CTAs per search (2 = cluster tier)
     bool mw = false;
     bool tm = false;         // TMEM tier (tm_batch_kernel): two 256-thread searches per SM, Delta in TMEM
+    bool tma = false;        // the asynchronous schedule on the TMEM tier (tm_async_kernel)
     bool tmw = false;        // TMEM warp tier (tmw_batch_kernel): 4 warp-searches per CTA, Delta in TMEM
     int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
     GaConst ga{};
@@ -256,8 +258,9 @@ static int batch_threads(const dabs_ctx* c) { return c->tm ? TM_NT : c->tmw ? 32
 static int batch_spc(const dabs_ctx* c) { return c->tmw ? TMW_SPC : 1; }
 
 using AsyncFn = void (*)(const AsyncArgs);
-static AsyncFn pick_async(int C, int NT, int CL)
+static AsyncFn pick_async(int C, int NT, int CL, bool tm = false)
 {
+    if (tm) return tm_async_kernel<0>;
     if (CL == 2) {
         switch (NT) {
         case 64: return async_kernel<8, 64, 2>;
@@ -285,6 +288,14 @@ static size_t row_smem_reg(const dabs_ctx* c)
 static size_t row_smem(const dabs_ctx* c)
 {
     return c->tm ? (size_t)2 * c->n_pad : c->tmw ? (size_t)2 * c->n_pad * TMW_SPC : row_smem_reg(c);
+}
+// the asynchronous schedule's persistent kernel, its threads and dynamic smem
+// (the row buffer doubles as the commit's scratch)
+static AsyncFn async_fn(const dabs_ctx* c) { return pick_async(c->C, c->NT, c->CL, c->tma); }
+static int async_threads(const dabs_ctx* c) { return c->tma ? TM_NT : c->NT; }
+static size_t async_smem(const dabs_ctx* c, int cap)
+{
+    return std::max(c->tma ? (size_t)2 * c->n_pad : row_smem_reg(c), async_commit_smem(cap));
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
@@ -401,7 +412,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         while (NT * 64 * c->CL < n) NT <<= 1;
         c->NT = NT;
         // 16384 < n <= 32768: the TMEM tier for the generation schedule (DABS_TMEM=0: the
-        // 512-thread register tier, A/B).  The asynchronous schedule keeps the register tier.
+        // 512-thread register tier, A/B).  The asynchronous schedule follows (tm_async_kernel).
         const char* et = getenv("DABS_TMEM");
         c->tm = c->CL == 1 && NT == 512 && !(et && et[0] == '0');
     }
@@ -418,8 +429,14 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
     {
-        cudaError_t e = cudaFuncSetAttribute(pick_async(c->C, c->NT, c->CL), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)std::max(row_smem_reg(c), async_commit_smem((int)cfg.pool_capacity)));
+        // the asynchronous schedule follows the tier (DABS_TMEM_ASYNC=0: the register tier at R32K)
+        const char* eta = getenv("DABS_TMEM_ASYNC");
+        c->tma = c->tm && !(eta && eta[0] == '0');
+        cudaError_t e = cudaFuncSetAttribute(async_fn(c), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)async_smem(c, (int)cfg.pool_capacity));
+        if (e == cudaSuccess && c->tma)
+            e = cudaFuncSetAttribute(async_fn(c), cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return bail(fail(DABS_E_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     }
     c->T = flip_factor(cfg.s_milli, n);
@@ -433,8 +450,8 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         int occ = 0;
         const bool one_wave = (cfg.flags & DABS_FLAG_ONE_WAVE) != 0;
         if (one_wave)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_async(c->C, c->NT, c->CL), c->NT,
-                                                          std::max(row_smem_reg(c), async_commit_smem((int)cfg.pool_capacity)));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, async_fn(c), async_threads(c),
+                                                          async_smem(c, (int)cfg.pool_capacity));
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pick_batch(c, false), batch_threads(c), row_smem(c));
         if (getenv("DABS_DEBUG_OCC")) fprintf(stderr, "dabs: occupancy %d CTAs/SM (tier NT=%d C=%d CL=%d tm=%d)\n", occ,
@@ -442,6 +459,7 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         // the TMEM tier is built for two co-resident searches per SM (ncu: 16
         // active warps per SM); the occupancy query reports one for it
         if (c->tm && !one_wave && occ < 2) occ = 2;
+        if (c->tma && one_wave && occ < 2) occ = 2;    // the same two co-resident searches per SM
         if (c->tmw && !one_wave && occ < 8) occ = 8;   // 8 CTAs x 4 searches: the TMEM columns and 64 registers
         if (occ < 1) occ = 1;
         // concurrent searches (the TMEM warp tier packs 4 per CTA)
@@ -1041,9 +1059,9 @@ extern "C" dabs_status dabs_run_async(dabs_ctx* c, uint64_t seed, uint64_t flip_
     a.bestE = c->a_bestE; a.bestX = c->a_bestX; a.brec = c->a_brec;
     a.profile = getenv("DABS_ASYNC_PHASES") ? 1 : 0;
     CK(cudaEventRecord(c->ev[1], s0));
-    const size_t asmem = std::max(row_smem_reg(c), async_commit_smem(c->cap));
+    const size_t asmem = async_smem(c, c->cap);
     if (c->CL == 1) {
-        pick_async(c->C, c->NT, 1)<<<c->slots, c->NT, asmem, s0>>>(a);
+        async_fn(c)<<<c->slots, async_threads(c), asmem, s0>>>(a);
         c->launches++;
     } else {
         cudaLaunchConfig_t lc = {};

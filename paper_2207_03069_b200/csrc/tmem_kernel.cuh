@@ -180,31 +180,19 @@ __device__ __forceinline__ int pick8(const int32_t (&v)[8], int e)
 __device__ unsigned long long g_tstat3[16];
 #endif
 
-template <bool TRACE>
-__global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
+// CTA-wide state that outlives one batch (the persistent asynchronous kernel
+// runs many): the TMEM allocation, the sigma table, the row mbarriers and
+// their phase parity
+__shared__ __align__(8) uint64_t tm_mbar_s[TM_NP];
+__shared__ uint32_t tm_tbase_s;
+__shared__ uint32_t tm_par_s;
+__shared__ uint4 tm_lut_s[256];   // sigma bytes of 8 elements as the four IDP.2A B words
+
+// once per CTA: 256 TMEM columns, the sigma table, the row mbarriers
+__device__ __forceinline__ void tm_cta_setup()
 {
-    constexpr int NT = TM_NT, lgNT = 8, C = TM_C, NW = NT / 32, NP = TM_NP, CPP = C / NP, CW = C / 2;
-    constexpr unsigned FULL = 0xffffffffu;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
-    const uint32_t gen = p.gen_ptr ? *p.gen_ptr : p.gen;
-    const uint32_t gslot = p.slot_base + (uint32_t)s;
-    const int n = p.n;
-
-    extern __shared__ __align__(128) uint8_t dyn_smem[];
-    const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // one W row, 2*n_pad bytes
-    __shared__ __align__(8) uint64_t mbar[NP];
-    __shared__ uint32_t tbase_s;
-    __shared__ int32_t ring_s[TABU_RING];
-    __shared__ int32_t red_s[2][32][RED_W];
-    __shared__ int32_t bc_s[2][4];
-    __shared__ int32_t sel_s[4];
-    __shared__ uint4 lut_s[256];      // sigma bytes of 8 elements as the four IDP.2A B words
-    __shared__ M128 pm_s[3][NT];      // [0] D bits, [1] M2, [2] BEST xor X
-    __shared__ int32_t cmin_s[C][NT]; // MaxMin / PositiveMin: per-chunk minima of the last scan
-
-    // ---------------- TMEM: 256 columns for this search
-    if (wid == 0) tm_alloc(&tbase_s, TM_COLS);
+    const int t = threadIdx.x, wid = t >> 5;
+    if (wid == 0) tm_alloc(&tm_tbase_s, TM_COLS);
     // sigma table: entry v = x bits of 8 elements, word j = (s_2j, 0, 0, s_2j+1),
     // s = 0x01 for x = 1 (+1), 0xFF for x = 0 (-1)
     {
@@ -215,17 +203,49 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
             const uint32_t s0 = ((v >> (2 * j)) & 1u) ? 0x01u : 0xFFu, s1 = ((v >> (2 * j + 1)) & 1u) ? 0x01u : 0xFFu;
             w[j] = s0 | (s1 << 24);
         }
-        lut_s[t] = make_uint4(w[0], w[1], w[2], w[3]);
+        tm_lut_s[t] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (t == 0) {
 #pragma unroll
-        for (int q = 0; q < NP; q++) mbar_init(&mbar[q], 1);
+        for (int q = 0; q < TM_NP; q++) mbar_init(&tm_mbar_s[q], 1);
         fence_mbar_init();
+        tm_par_s = 0;
     }
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    const uint32_t tw = tbase_s + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));   // this warp's base
+}
+__device__ __forceinline__ void tm_cta_teardown()
+{
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    if ((threadIdx.x >> 5) == 0) tm_dealloc(tm_tbase_s, TM_COLS);
+}
+
+// One batch search of slot s with Delta in TMEM.  REUSE: the CTA
+// runs further batches (persistent asynchronous kernel): packets written by
+// the commit warp are read from L2, the row mbarriers' parity carries over.
+template <bool TRACE, bool REUSE>
+__device__ __forceinline__ void tm_batch_body(const BatchParams& p, const int s, const uint32_t gen)
+{
+    constexpr int NT = TM_NT, lgNT = 8, C = TM_C, NW = NT / 32, NP = TM_NP, CPP = C / NP, CW = C / 2;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const uint32_t gslot = p.slot_base + (uint32_t)s;
+    const int n = p.n;
+
+    extern __shared__ __align__(128) uint8_t dyn_smem[];
+    const uint4* row_s = reinterpret_cast<const uint4*>(dyn_smem);   // one W row, 2*n_pad bytes
+    uint64_t* mbar = tm_mbar_s;
+    const uint4* lut_s = tm_lut_s;
+    __shared__ int32_t ring_s[TABU_RING];
+    __shared__ int32_t red_s[2][32][RED_W];
+    __shared__ int32_t bc_s[2][4];
+    __shared__ int32_t sel_s[4];
+    __shared__ M128 pm_s[3][NT];      // [0] D bits, [1] M2, [2] BEST xor X
+    __shared__ int32_t cmin_s[C][NT]; // MaxMin / PositiveMin: per-chunk minima of the last scan
+    const uint32_t tw = tm_tbase_s + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));   // this warp's base
 
     // ---------------- load the slot's persistent state (R-14)
     M128 xb{0, 0}, vb{0, 0};
@@ -242,7 +262,7 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
                 const int c = q * CPP + cc;
                 const int ch = (c << lgNT) + t;
                 mor_byte(xb, c, Xb[ch]);
-                mor_byte(db, c, Db[ch]);
+                mor_byte(db, c, REUSE ? __ldcg(Db + ch) : Db[ch]);
                 const int nv = min(max(n - ch * 8, 0), 8);
                 mor_byte(vb, c, (1u << nv) - 1u);
                 const int4 a = reinterpret_cast<const int4*>(dp + ch * 8)[0];
@@ -256,13 +276,13 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
         pm_s[2][t] = M128{0, 0};
     }
     tm_wait_st();
-    if (t < TABU_RING) ring_s[t] = p.ring[(size_t)s * TABU_RING + t];
+    if (t < TABU_RING) ring_s[t] = REUSE ? __ldcg(p.ring + (size_t)s * TABU_RING + t) : p.ring[(size_t)s * TABU_RING + t];
     int pos = 0;   // ring_s[(pos + j) & 31] = j-th most recent flip
-    int64_t E = p.E[s];
-    const int algo = (int)p.algo[s];
+    int64_t E = REUSE ? (int64_t)__ldcg(reinterpret_cast<const long long*>(p.E + s)) : p.E[s];
+    const int algo = REUSE ? (int)__ldcg(p.algo + s) : (int)p.algo[s];
     const int tabu = p.tabu;
     const int T = p.T;
-    uint32_t par_row = 0;
+    uint32_t par_row = tm_par_s;   // 0 at every launch; carried across batches (REUSE)
     int flips = 0;
     int64_t ebest = E_INF;
     int rc = 0;
@@ -917,10 +937,17 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
         for (int j = 0; j < 16; j++) atomicAdd(&g_tstat3[j], ts3_s[j]);
 #endif
 #undef DABS_T3
-    tm_fence_before();
-    __syncthreads();
-    tm_fence_after();
-    if (wid == 0) tm_dealloc(tbase_s, TM_COLS);
+    __syncthreads();                 // every thread read tm_par_s at the start
+    if (t == 0) tm_par_s = par_row;
+}
+
+template <bool TRACE>
+__global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
+{
+    tm_cta_setup();
+    const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
+    tm_batch_body<TRACE, false>(p, s, p.gen_ptr ? *p.gen_ptr : p.gen);
+    tm_cta_teardown();
 }
 
 }  // namespace dabs

@@ -7,7 +7,7 @@ cases: async   -- dabs_run_async, n = 96, 2 pools, one wave (ticket locks, pool 
                   TMA rows, CTA exchange): a batch to a local minimum, then a short checked batch
                   (sanitize only the 2nd launch: --kernel-name kns=batch_kernel --launch-skip 1
                   --launch-count 1)
-       ctareg  -- the same on the 512-thread register tier (DABS_TMEM=0, kept by the async schedule)
+       ctareg  -- the same on the 512-thread register tier (DABS_TMEM=0)
        tmw     -- generations on the TMEM warp tier (DABS_TMW=1), n = 1000
        warp    -- generations on the warp tier, n = 1000
 Each case also checks its result against the CPU oracle (so a run that the
