@@ -109,7 +109,8 @@ void dabs_config_default(dabs_config* cfg);
  * read for the model; any nonzero below the diagonal -> DABS_E_TRIANGLE.
  * 1 <= n <= 65536 else DABS_E_ARG (n <= 2048: one warp per search; n <=
  * 16384: one CTA; n <= 32768: one 256-thread CTA with Delta in tensor memory,
- * two per SM; n > 32768: a cluster of two CTAs).  T = ceil(s n) > 65536
+ * two per SM; n > 32768: one 512-thread CTA per SM with Delta in all of its
+ * tensor memory, or a cluster of two CTAs with DABS_TMEM64=0).  T = ceil(s n) > 65536
  * or B = ceil(b n) > 2^30 -> DABS_E_ARG (the exact MaxMin span and the
  * flip counters are sized for those).  eps_ppm = 1000000 means "always
  * uniform" (R-15).  If max_k (|W_kk| +

@@ -67,6 +67,7 @@ struct dabs_ctx {
     int CL = 1;              // CTAs per search (2 = cluster tier)
     bool mw = false;
     bool tm = false;         // TMEM tier (tm_batch_kernel): two 256-thread searches per SM, Delta in TMEM
+    int tmNT = 256;          // its threads per search: 256 (n <= 32768) or 512 (n > 32768, DABS_TMEM64=1)
     bool tma = false;        // the asynchronous schedule on the TMEM tier (tm_async_kernel)
     bool tmw = false;        // TMEM warp tier (tmw_batch_kernel): 4 warp-searches per CTA, Delta in TMEM
     int T = 0, B = 0, tabu = 8, cap = 100, P = 1, S = 1, slots = 1;
@@ -245,7 +246,10 @@ static BatchFn pick_batch(int C, int NT, int CL, bool trace)
 }
 static BatchFn pick_batch(const dabs_ctx* c, bool trace)
 {
-    if (c->tm) return trace ? tm_batch_kernel<true> : tm_batch_kernel<false>;
+    if (c->tm) {
+        if (c->tmNT == 512) return trace ? tm_batch_kernel<512, true> : tm_batch_kernel<512, false>;
+        return trace ? tm_batch_kernel<256, true> : tm_batch_kernel<256, false>;
+    }
     if (c->tmw) {
         if (c->C == 8) return trace ? tmw_batch_kernel<8, true> : tmw_batch_kernel<8, false>;
         return trace ? tmw_batch_kernel<4, true> : tmw_batch_kernel<4, false>;
@@ -253,14 +257,14 @@ static BatchFn pick_batch(const dabs_ctx* c, bool trace)
     return pick_batch(c->C, c->NT, c->CL, trace);
 }
 // threads per CTA of the generation schedule's batch kernel
-static int batch_threads(const dabs_ctx* c) { return c->tm ? TM_NT : c->tmw ? 32 * TMW_SPC : c->NT; }
+static int batch_threads(const dabs_ctx* c) { return c->tm ? c->tmNT : c->tmw ? 32 * TMW_SPC : c->NT; }
 // searches per CTA of the generation schedule's batch kernel
 static int batch_spc(const dabs_ctx* c) { return c->tmw ? TMW_SPC : 1; }
 
 using AsyncFn = void (*)(const AsyncArgs);
 static AsyncFn pick_async(int C, int NT, int CL, bool tm = false)
 {
-    if (tm) return tm_async_kernel<0>;
+    if (tm) return NT == 512 ? tm_async_kernel<512> : tm_async_kernel<256>;
     if (CL == 2) {
         switch (NT) {
         case 64: return async_kernel<8, 64, 2>;
@@ -287,15 +291,15 @@ static size_t row_smem_reg(const dabs_ctx* c)
 // the generation schedule's batch kernel: the TMEM tier keeps only the W row in dynamic smem
 static size_t row_smem(const dabs_ctx* c)
 {
-    return c->tm ? (size_t)2 * c->n_pad : c->tmw ? (size_t)2 * c->n_pad * TMW_SPC : row_smem_reg(c);
+    return c->tm ? tm_dyn_smem(c->n_pad, c->tmNT) : c->tmw ? (size_t)2 * c->n_pad * TMW_SPC : row_smem_reg(c);
 }
 // the asynchronous schedule's persistent kernel, its threads and dynamic smem
 // (the row buffer doubles as the commit's scratch)
-static AsyncFn async_fn(const dabs_ctx* c) { return pick_async(c->C, c->NT, c->CL, c->tma); }
-static int async_threads(const dabs_ctx* c) { return c->tma ? TM_NT : c->NT; }
+static AsyncFn async_fn(const dabs_ctx* c) { return pick_async(c->C, c->tma ? c->tmNT : c->NT, c->CL, c->tma); }
+static int async_threads(const dabs_ctx* c) { return c->tma ? c->tmNT : c->NT; }
 static size_t async_smem(const dabs_ctx* c, int cap)
 {
-    return std::max(c->tma ? (size_t)2 * c->n_pad : row_smem_reg(c), async_commit_smem(cap));
+    return std::max(c->tma ? tm_dyn_smem(c->n_pad, c->tmNT) : row_smem_reg(c), async_commit_smem(cap));
 }
 
 static BatchParams batch_params(dabs_ctx* c, uint64_t seed, uint32_t gen, int slot0)
@@ -407,7 +411,12 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         c->mw = true;
         c->C = 8;
         const char* ev = getenv("DABS_CLUSTER");
-        c->CL = (n > 32768 || (ev && ev[0] == '1' && n > 4096)) ? 2 : 1;
+        const char* e64 = getenv("DABS_TMEM64");
+        // n > 32768: one 512-thread CTA per SM with all of Delta (256 KB) in the SM's
+        // tensor memory (R64K 0.371 -> 0.661 of HBM against the cluster tier,
+        // tools/gpu_tm64.sh); DABS_TMEM64=0 or DABS_CLUSTER=1: the 2-CTA cluster tier
+        const bool tm64 = n > 32768 && !(e64 && e64[0] == '0') && !(ev && ev[0] == '1');
+        c->CL = ((n > 32768 && !tm64) || (ev && ev[0] == '1' && n > 4096)) ? 2 : 1;
         int NT = 64;
         while (NT * 64 * c->CL < n) NT <<= 1;
         c->NT = NT;
@@ -415,6 +424,12 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
         // 512-thread register tier, A/B).  The asynchronous schedule follows (tm_async_kernel).
         const char* et = getenv("DABS_TMEM");
         c->tm = c->CL == 1 && NT == 512 && !(et && et[0] == '0');
+        if (tm64) {
+            c->tm = true;
+            c->tmNT = 512;
+            c->NT = 512;
+            c->C = 16;                    // 512 threads x 128 elements: n_pad = 65536
+        }
     }
     c->n_pad = c->NT * c->CL * c->C * 8;
     c->nwp = c->n_pad / 32;
@@ -458,8 +473,8 @@ static dabs_status create_begin(int32_t n, const dabs_config* cfg_in, dabs_ctx**
                                              batch_threads(c), c->C, c->CL, (int)c->tm);
         // the TMEM tier is built for two co-resident searches per SM (ncu: 16
         // active warps per SM); the occupancy query reports one for it
-        if (c->tm && !one_wave && occ < 2) occ = 2;
-        if (c->tma && one_wave && occ < 2) occ = 2;    // the same two co-resident searches per SM
+        if (c->tm && c->tmNT == 256 && !one_wave && occ < 2) occ = 2;
+        if (c->tma && c->tmNT == 256 && one_wave && occ < 2) occ = 2;    // the same two co-resident searches per SM
         if (c->tmw && !one_wave && occ < 8) occ = 8;   // 8 CTAs x 4 searches: the TMEM columns and 64 registers
         if (occ < 1) occ = 1;
         // concurrent searches (the TMEM warp tier packs 4 per CTA)

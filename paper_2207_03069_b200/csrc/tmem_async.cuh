@@ -10,16 +10,16 @@
 
 namespace dabs {
 
-template <int DUMMY>
-__global__ void __launch_bounds__(TM_NT, 2) tm_async_kernel(const AsyncArgs a)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tm_async_kernel(const AsyncArgs a)
 {
     const int s = (int)blockIdx.x;
     const unsigned long long t_start = globaltimer();
     unsigned long long t_body = 0, t_commit = 0;
-    tm_cta_setup();
+    tm_cta_setup<NT>();
     for (uint32_t k = 0;; k++) {
         const unsigned long long tb = globaltimer();
-        tm_batch_body<false, true>(a.bp, s, k);
+        tm_batch_body<NT, false, true>(a.bp, s, k);
         __syncthreads();
         const unsigned long long tc = globaltimer();
         t_body += tc - tb;
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(TM_NT, 2) tm_async_kernel(const AsyncArgs a)
         t_commit += globaltimer() - tc;
         if (!more) break;
     }
-    tm_cta_teardown();
+    tm_cta_teardown<NT>();
     if (a.profile && threadIdx.x == 0) {
         atomicAdd(a.lock_ns + 7, t_body);                    // time in batches
         atomicAdd(a.lock_ns + 8, globaltimer() - t_start);   // CTA lifetime

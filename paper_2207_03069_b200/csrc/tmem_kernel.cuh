@@ -25,10 +25,12 @@
 
 namespace dabs {
 
-constexpr int TM_NT = 256;   // threads per search
+constexpr int TM_NT = 256;   // threads per search (R32K tier; the n > 32768 variant runs 512)
 constexpr int TM_C = 16;     // chunks of 8 elements per thread
 constexpr int TM_NP = 4;     // W-row pieces per flip (one mbarrier each)
-constexpr int TM_COLS = 256; // TMEM columns per CTA
+constexpr int TM_COLS = 256; // TMEM columns per CTA (= threads per search)
+// dynamic shared memory of a TMEM-tier CTA: the W row, then the mask and chunk-minimum arrays
+inline size_t tm_dyn_smem(int n_pad, int nt) { return 2 * (size_t)n_pad + (3 * 16 + TM_C * 4) * (size_t)nt; }
 
 // ---------------------------------------------------------------- tcgen05 helpers
 __device__ __forceinline__ void tm_alloc(uint32_t* dst_smem, uint32_t ncols)
@@ -188,11 +190,12 @@ __shared__ uint32_t tm_tbase_s;
 __shared__ uint32_t tm_par_s;
 __shared__ uint4 tm_lut_s[256];   // sigma bytes of 8 elements as the four IDP.2A B words
 
-// once per CTA: 256 TMEM columns, the sigma table, the row mbarriers
+// once per CTA: NT TMEM columns, the sigma table, the row mbarriers
+template <int NT>
 __device__ __forceinline__ void tm_cta_setup()
 {
     const int t = threadIdx.x, wid = t >> 5;
-    if (wid == 0) tm_alloc(&tm_tbase_s, TM_COLS);
+    if (wid == 0) tm_alloc(&tm_tbase_s, NT);
     // sigma table: entry v = x bits of 8 elements, word j = (s_2j, 0, 0, s_2j+1),
     // s = 0x01 for x = 1 (+1), 0xFF for x = 0 (-1)
     {
@@ -203,7 +206,7 @@ __device__ __forceinline__ void tm_cta_setup()
             const uint32_t s0 = ((v >> (2 * j)) & 1u) ? 0x01u : 0xFFu, s1 = ((v >> (2 * j + 1)) & 1u) ? 0x01u : 0xFFu;
             w[j] = s0 | (s1 << 24);
         }
-        tm_lut_s[t] = make_uint4(w[0], w[1], w[2], w[3]);
+        if (t < 256) tm_lut_s[t] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (t == 0) {
 #pragma unroll
@@ -215,21 +218,24 @@ __device__ __forceinline__ void tm_cta_setup()
     __syncthreads();
     tm_fence_after();
 }
+template <int NT>
 __device__ __forceinline__ void tm_cta_teardown()
 {
     tm_fence_before();
     __syncthreads();
     tm_fence_after();
-    if ((threadIdx.x >> 5) == 0) tm_dealloc(tm_tbase_s, TM_COLS);
+    if ((threadIdx.x >> 5) == 0) tm_dealloc(tm_tbase_s, NT);
 }
 
 // One batch search of slot s with Delta in TMEM.  REUSE: the CTA
 // runs further batches (persistent asynchronous kernel): packets written by
 // the commit warp are read from L2, the row mbarriers' parity carries over.
-template <bool TRACE, bool REUSE>
+// NT = 256 (n <= 32768, 256 TMEM columns, two CTAs per SM) or 512 (n <= 65536,
+// all 512 columns, one CTA per SM); warp w: lanes 32(w%4).., columns 128(w/4)..
+template <int NT, bool TRACE, bool REUSE>
 __device__ __forceinline__ void tm_batch_body(const BatchParams& p, const int s, const uint32_t gen)
 {
-    constexpr int NT = TM_NT, lgNT = 8, C = TM_C, NW = NT / 32, NP = TM_NP, CPP = C / NP, CW = C / 2;
+    constexpr int lgNT = NT == 512 ? 9 : 8, C = TM_C, NW = NT / 32, NP = TM_NP, CPP = C / NP, CW = C / 2;
     constexpr unsigned FULL = 0xffffffffu;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const uint32_t gslot = p.slot_base + (uint32_t)s;
@@ -243,8 +249,10 @@ __device__ __forceinline__ void tm_batch_body(const BatchParams& p, const int s,
     __shared__ int32_t red_s[2][32][RED_W];
     __shared__ int32_t bc_s[2][4];
     __shared__ int32_t sel_s[4];
-    __shared__ M128 pm_s[3][NT];      // [0] D bits, [1] M2, [2] BEST xor X
-    __shared__ int32_t cmin_s[C][NT]; // MaxMin / PositiveMin: per-chunk minima of the last scan
+    // after the row in dynamic shared memory (48 KB static limit at NT = 512):
+    // [0] D bits, [1] M2, [2] BEST xor X; MaxMin / PositiveMin chunk minima of the last scan
+    M128 (*pm_s)[NT] = reinterpret_cast<M128 (*)[NT]>(dyn_smem + 2 * (size_t)p.n_pad);
+    int32_t (*cmin_s)[NT] = reinterpret_cast<int32_t (*)[NT]>(dyn_smem + 2 * (size_t)p.n_pad + 3 * NT * sizeof(M128));
     const uint32_t tw = tm_tbase_s + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)(128 * (wid >> 2));   // this warp's base
 
     // ---------------- load the slot's persistent state (R-14)
@@ -941,13 +949,13 @@ __device__ __forceinline__ void tm_batch_body(const BatchParams& p, const int s,
     if (t == 0) tm_par_s = par_row;
 }
 
-template <bool TRACE>
-__global__ void __launch_bounds__(TM_NT, 2) tm_batch_kernel(const BatchParams p)
+template <int NT, bool TRACE>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1) tm_batch_kernel(const BatchParams p)
 {
-    tm_cta_setup();
+    tm_cta_setup<NT>();
     const int s = p.order ? p.order[blockIdx.x] : p.slot0 + (int)blockIdx.x;
-    tm_batch_body<TRACE, false>(p, s, p.gen_ptr ? *p.gen_ptr : p.gen);
-    tm_cta_teardown();
+    tm_batch_body<NT, TRACE, false>(p, s, p.gen_ptr ? *p.gen_ptr : p.gen);
+    tm_cta_teardown<NT>();
 }
 
 }  // namespace dabs

@@ -137,6 +137,36 @@ def test_async_full_config_tsp32(orc, lib):
     assert (Eg, Xg.tobytes()) == (w.best()[0], w.best()[1].tobytes())
 
 
+def test_async_r64k_sampled(orc, lib):
+    """n = 65536 (8 GiB W) on the TMEM tier's persistent kernel (one 512-thread
+    CTA per SM, Delta in all 512 TMEM columns): with a budget of one flip every
+    slot runs exactly its batch 0 from X = 0; two slots recomputed by the oracle."""
+    from paper_2207_03069_b200 import workloads as wl
+    U, meta = wl.make("R64K", seed=1)
+    solver = lib.Solver(U, s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1, one_wave=True)
+    assert solver.stats().threads_per_search == 512
+    solver.run_async(13, 1)
+    log = solver.async_log()
+    assert len(log) == solver.slots and not (log & (SEEDED | XREAD)).any()
+    w = orc.World(U, orc.Config(s_milli=meta["s_milli"], b_milli=meta["b_milli"], pools=1, slots=solver.slots))
+    w.reset(13)
+    w.async_begin()
+    for s in (0, solver.slots - 1):
+        opk = w.packet(s)
+        gpk = solver.read_packet(s)
+        np.testing.assert_array_equal(gpk["D"], opk["D"])
+        assert gpk["algo"] == opk["algo"]
+        st = orc.SlotState.initial(U)
+        ref = orc.batch(U, st, opk["D"], opk["algo"], T=solver.T, B=solver.B, tabu=8, seed=13, slot=s, gen=0)
+        assert ref.flips == gpk["flips"] and ref.ebest == gpk["ebest"]
+        np.testing.assert_array_equal(ref.best, gpk["best"])
+        post = solver.read_slot(s)
+        np.testing.assert_array_equal(st.x, post["x"])
+        np.testing.assert_array_equal(st.delta, post["delta"])
+        assert st.E == post["E"]
+    solver.close()
+
+
 def test_async_r32k_sampled(orc, lib):
     """R32K at full size (2 GiB W), one wave of 148 persistent searches: with a
     budget of one flip every slot runs exactly its batch 0 (from X = 0, packet

@@ -130,16 +130,19 @@ def r64k():
     return wl.make("R64K", seed=1)[0]
 
 
+@pytest.mark.parametrize("tier", ["cluster", "tmem64"])
 @pytest.mark.parametrize("n", [32769, 65536])
-def test_batch_parity_large_n(orc, lib, r64k, n):
-    """n > 32768 always runs on the cluster tier.  Short batches (s = b =
-    0.001, D = X with 40 bits changed) keep the oracle at seconds per batch;
-    the search starts at X = 0 (Delta = diag)."""
+def test_batch_parity_large_n(orc, lib, r64k, monkeypatch, tier, n):
+    """n > 32768: one 512-thread CTA per SM with all of Delta (256 KB) in tensor
+    memory (the default), or the cluster tier (DABS_TMEM64=0, two CTAs per search).
+    Short batches (s = b = 0.001, D = X with 40 bits changed) keep the oracle
+    at seconds per batch; the search starts at X = 0 (Delta = diag)."""
     from paper_2207_03069_b200 import workloads as wl
+    monkeypatch.setenv("DABS_TMEM64", "1" if tier == "tmem64" else "0")
     rng = np.random.default_rng(3000 + n)
     U = r64k if n == 65536 else wl.random_dense(n, seed=n, lo=-3000, hi=3000)
     solver = lib.Solver(U, s_milli=1, b_milli=1, pools=1, slots=1)
-    assert solver.stats().threads_per_search == 1024
+    assert solver.stats().threads_per_search == (1024 if tier == "cluster" else 512)
     st0 = orc.SlotState.initial(U)
     for algo in ALGS:
         st = st0.copy()
